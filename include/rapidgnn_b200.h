@@ -1,0 +1,202 @@
+/*
+ * rapidgnn_b200.h — C ABI of the B200 hot path for RapidGNN's data path
+ * (reference: gnnpipe, /root/reference/pkg/src/gnnpipe).
+ *
+ * The reference is pure Python/numpy and has no FFI of its own: its
+ * boundary is the module API re-exported by gnnpipe/__init__.py:5-19.  Each
+ * entry point below is the device kernel behind one of those functions;
+ * paper_2505_10806_b200/ (Python, ctypes) mirrors the reference API on top
+ * of it (see INTEGRATION.md for the binding a maintainer would add).
+ *
+ * Conventions
+ *   - every function returns 0 (RG_OK) or a negative RG_ERR_* code and never
+ *     throws; rg_last_error() returns a thread-local message for the last
+ *     failure on the calling thread;
+ *   - pointers named d_* are device pointers, h_* host pointers; all device
+ *     buffers are caller-owned, nothing allocates behind the caller's back;
+ *   - work is enqueued on the caller's stream (cudaStream_t passed as void*),
+ *     no entry point synchronises the host, so every call is capturable in a
+ *     CUDA graph;
+ *   - node ids are int32 on device (every configured graph has n < 2^31),
+ *     CSR row pointers int64;
+ *   - "group" = G mini-batches processed by one launch; per-batch buffers are
+ *     G fixed-capacity slots laid out back to back (slot b at b * cap).
+ */
+#ifndef RAPIDGNN_B200_H
+#define RAPIDGNN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RG_OK 0
+#define RG_ERR_INVALID (-1)     /* bad argument (maps to ValueError)          */
+#define RG_ERR_CUDA (-2)        /* CUDA runtime / launch failure              */
+#define RG_ERR_UNSUPPORTED (-3) /* shape outside what the kernels support     */
+#define RG_ERR_NOT_OWNED (-4)   /* pull for an id the shard does not own      */
+
+/* route word of a node, one uint32 per node:
+ *   bits 28..31 = source kind: partition id 0..14, or RG_KIND_CACHE
+ *   bits  0..27 = row index inside that partition's shard / the cache   */
+#define RG_KIND_SHIFT 28
+#define RG_KIND_CACHE 15u
+#define RG_ROW_MASK 0x0FFFFFFFu
+#define RG_ROUTE_INVALID 0xFFFFFFFFu
+#define RG_MAX_PARTS 15
+
+/* per-batch bundle counters written by rg_gather_bundle (uint32 each)   */
+#define RG_CNT_LOCAL 0
+#define RG_CNT_HIT 1
+#define RG_CNT_FALLBACK 2
+#define RG_CNT_OWNER_MASK 3 /* bit q set <=> >=1 fallback row owned by q */
+#define RG_CNT_BAD 4        /* rows whose route was RG_ROUTE_INVALID     */
+#define RG_NCOUNTERS 8
+
+const char* rg_last_error(void);
+int rg_abi_version(void);
+/* 1 if the library was built for sm_100a and a device is usable, else 0 */
+int rg_device_ok(void);
+
+/* ---- L1 randomness (rng.py:28-62) ----------------------------------- */
+/* out[i] = mix64(in[i])                              rng.py:28-44       */
+int rg_mix64(const uint64_t* d_in, uint64_t* d_out, int64_t n, void* stream);
+/* out[j] = mix64((j+1)*GOLDEN + master), j < count  rng.py:47-50       */
+int rg_stream_keys(uint64_t master, int64_t count, uint64_t* d_out, void* stream);
+
+/* ---- L2 sampling (sampler.py:86-152) -------------------------------- */
+/* Seeds of batches i0..i0+G-1 of an epoch permutation (chunks of
+ * batch_size, last one partial; sampler.py:57) into d_seeds (G x seed_cap)
+ * / d_nseeds, and rng[b] = mix64(s0 ^ (epoch<<32 | i0+b)) (sampler.py:40).*/
+int rg_fill_seeds(const int32_t* d_perm, int64_t n_perm, int32_t batch_size, int64_t i0,
+                  int32_t G, int32_t* d_seeds, int32_t* d_nseeds, int32_t seed_cap, uint64_t s0,
+                  int64_t epoch, uint64_t* d_rng, void* stream);
+
+/* Level-0 frontier: mark the seeds of every batch in its bitmap.
+ * d_seeds: G x seed_cap int32, d_nseeds: G int32; d_bm: G x nwords.
+ * (np.unique(seeds), sampler.py:138, is the compaction that follows.)  */
+int rg_mark_seeds(const int32_t* d_seeds, const int32_t* d_nseeds, int32_t G, int32_t seed_cap,
+                  uint32_t* d_bm, int64_t nwords, void* stream);
+
+/* One expansion step d for G batches (sampler.py:86-113 + 145-148).
+ * For frontier node j of batch b (v = front[b*cap_in + j]):
+ *   take = min(deg v, fanout); the take positions with the smallest
+ *   SplitMix64 keys mix(nk + (p+1)G), nk = mix((v+1)G ^ s_d),
+ *   s_d = mix(rng_seed[b] ^ (level+1)G), are selected; their neighbour ids,
+ *   ascending, go to ell[b*cap_in*fanout + j*fanout + r], r < take, and
+ *   cnt[b*cap_in + j] = take.  Each selected neighbour id is OR-ed into the
+ *   batch bitmap, so after the step bm = F_d U src (sampler.py:148).
+ * d_slow: scratch of 1 + G*cap_in int32, required only when fanout > 32
+ * (rows with take > 32 go to a CTA-per-row path); fanout <= 4096.     */
+int rg_sample_level(const int64_t* d_indptr, const int32_t* d_indices, int64_t n,
+                    int32_t G, const int32_t* d_front, int64_t cap_in, const int32_t* d_nfront,
+                    int32_t fanout, int32_t level, const uint64_t* d_rng_seed, int32_t* d_ell,
+                    int32_t* d_cnt, uint32_t* d_bm, int64_t nwords, int32_t* d_slow,
+                    void* stream);
+
+/* Sorted-unique compaction of G bitmaps (np.unique / np.union1d).
+ * Writes ascending ids of set bits to out[b*cap_out ...], count to
+ * d_nout[b].  d_chunk: G x rg_bitmap_chunks(nwords) int32 scratch.
+ * If d_wpre != NULL it also receives the exclusive popcount prefix per
+ * word (G x nwords), i.e. rank(v) = wpre[v>>5] + popc(bm & lowmask). */
+int64_t rg_bitmap_chunks(int64_t nwords);
+int rg_bitmap_compact(const uint32_t* d_bm, int64_t nwords, int32_t G, int32_t* d_chunk,
+                      int32_t* d_out, int64_t cap_out, int32_t* d_nout, int32_t* d_wpre,
+                      void* stream);
+/* set bit v for every v in ids[0..n) (single bitmap)                   */
+int rg_bitmap_set(const int32_t* d_ids, const int32_t* d_n, uint32_t* d_bm, void* stream);
+
+/* ELL block level -> flat (src, dst) edge list in (dst, src) order, as
+ * ComputationBlock.edges[d] (sampler.py:145-146).  d_eoff (G x (cap_in+1))
+ * receives per-dst offsets, d_nedge[b] the edge count; src/dst written at
+ * b*cap_e.  d_chunk: G x rg_scan_chunks(cap_in) scratch.            */
+int64_t rg_scan_chunks(int64_t cap);
+int rg_ell_to_edges(const int32_t* d_front, const int32_t* d_nfront, int64_t cap_in,
+                    const int32_t* d_ell, const int32_t* d_cnt, int32_t fanout, int32_t G,
+                    int32_t* d_chunk, int32_t* d_eoff, int32_t* d_src, int32_t* d_dst,
+                    int64_t cap_e, int32_t* d_nedge, void* stream);
+
+/* ---- L3 planning (plan.py:108-141) ---------------------------------- */
+/* counts[v] += number of the G batch bitmaps holding v (one access per
+ * batch appearance, plan.py:117-130 before the remote mask).          */
+int rg_count_inputs(const uint32_t* d_bm, int64_t nwords, int32_t G, int64_t n,
+                    uint32_t* d_counts, void* stream);
+/* candidates: route kind != my_part and counts[v] > 0.
+ * hist[c] += 1 for each candidate with count c (c clamped to max_count);
+ * d_bm_cand receives the candidate bitmap.                            */
+int rg_count_histogram(const uint32_t* d_counts, const uint8_t* d_owner, int32_t my_part,
+                       int64_t n, uint32_t* d_hist, int32_t max_count, uint32_t* d_bm_cand,
+                       void* stream);
+/* threshold split for top_hot (plan.py:133-141): bm_gt = candidates with
+ * count > c_star, bm_eq = candidates with count == c_star.             */
+int rg_threshold_split(const uint32_t* d_counts, const uint32_t* d_bm_cand, int64_t n,
+                       uint32_t c_star, uint32_t* d_bm_gt, uint32_t* d_bm_eq, void* stream);
+/* out[i] = counts[ids[i]] (FrequencyTable.counts)                      */
+int rg_gather_counts(const uint32_t* d_counts, const int32_t* d_ids, const int32_t* d_n,
+                     int64_t cap, uint32_t* d_out, void* stream);
+
+/* ---- L4 feature path (cache.py, store.py, prefetch.py) -------------- */
+/* route[v] = RG_KIND_CACHE<<28 | i for v = hot[i] (i < n_hot), copied from
+ * base_route elsewhere: the slot map of FeatureCache (cache.py:54-78). */
+int rg_route_with_cache(const uint32_t* d_base_route, int64_t n, const int32_t* d_hot,
+                        int64_t n_hot, uint32_t* d_route, void* stream);
+
+/* Feature bundle gather for G batches (prefetch.py:41-88, cache.py:54-78,
+ * store.py:66-69,173-196).  Row j of batch b is copied bit-exactly from
+ *   bases[kind] + (route[id] & RG_ROW_MASK) * stride
+ * to out[(b*cap + j) * stride], kind = route >> 28 (partition shard or
+ * cache).  Classification per row: kind == my_part -> local, kind ==
+ * RG_KIND_CACHE -> cache hit, else fallback pull from shard `kind`.
+ * d_counters: G x RG_NCOUNTERS uint32, accumulated (caller zeroes).
+ * h_bases: host array of 16 device pointers (peer pointers allowed);
+ * stride = row stride in floats, multiple of 4 (16-byte rows).        */
+int rg_gather_bundle(const int32_t* d_ids, const int32_t* d_nids, int64_t cap, int32_t G,
+                     const uint32_t* d_route, const float* const* h_bases, int32_t stride,
+                     int32_t my_part, float* d_out, uint32_t* d_counters, void* stream);
+
+/* ---- L5 aggregation consumer (model.py:72-81, 126-135) -------------- */
+/* mean[t] = (sum over t's edges, in stored order, of h[pos(src)]) /
+ * max(cnt_t, 1) and self[t] = h[pos(dst_front[t])], positions located by
+ * binary search in the sorted src_front.  fp32, in-order, IEEE divide. */
+int rg_sage_mean_fwd(const float* d_h, int64_t n_src, int32_t H, int32_t ldh,
+                     const int32_t* d_src_front, const int32_t* d_dst_front, int64_t n_dst,
+                     const int32_t* d_ell, const int32_t* d_cnt, int32_t fanout, float* d_mean,
+                     float* d_self, int32_t* d_self_pos, void* stream);
+/* Backward scatter (model.py:126-135): dh = 0; dh[self_pos[t]] += dself[t];
+ * then for each edge in (dst asc, src asc) order dh[pos(src)] +=
+ * dmean[t] / max(cnt_t,1).  d_tpos/d_toff: transposed edge index built
+ * by rg_sage_transpose (same order => deterministic, bit-exact).       */
+int64_t rg_sage_transpose_scratch(int64_t n_src, int64_t n_dst, int32_t fanout);
+int rg_sage_transpose(const int32_t* d_src_front, int64_t n_src, const int32_t* d_ell,
+                      const int32_t* d_cnt, int64_t n_dst, int32_t fanout, int32_t* d_toff,
+                      int32_t* d_tdst, int32_t* d_scratch, void* stream);
+/* d_self_of: n_src int32 scratch                                        */
+int rg_sage_mean_bwd(const float* d_dself, const float* d_dmean, int64_t n_dst, int32_t H,
+                     const int32_t* d_cnt, const int32_t* d_self_pos, const int32_t* d_toff,
+                     const int32_t* d_tdst, int64_t n_src, int32_t* d_self_of, float* d_dh,
+                     void* stream);
+
+/* ---- host-side graph materialisation (graph.py, partition.py) ------- */
+int rg_philox_raw(uint64_t key0, uint64_t key1, int64_t count, uint64_t* h_out);
+/* CSR of gnnpipe.graph.synth_powerlaw(n, m, ., ., seed) with the Philox
+ * key numpy derives from seed; h_indptr n+1, h_indices 2*m*(n-m).
+ * h_state13 (optional) receives the generator state after the attachment
+ * loop: counter[4], key[2], buffer[4], buffer_pos, has_uint32, uinteger,
+ * so the caller can continue the same numpy stream (features, masks).  */
+int rg_synth_powerlaw_csr(int64_t n, int64_t m, uint64_t key0, uint64_t key1, int64_t* h_indptr,
+                          int32_t* h_indices, uint64_t* h_state13);
+/* gnnpipe.partition.partition_edgecut(g, k).owner                     */
+int rg_partition_edgecut(int64_t n, const int64_t* h_indptr, const int32_t* h_indices, int32_t k,
+                         int32_t* h_owner);
+
+/* ---- multi-GPU plumbing: CUDA IPC for peer shard pointers ----------- */
+/* handle of the allocation holding d_ptr, and d_ptr's offset inside it */
+int rg_ipc_handle(const void* d_ptr, uint8_t* h_handle64, int64_t* h_offset);
+int rg_ipc_open(const uint8_t* h_handle64, void** d_ptr_out);
+int rg_ipc_close(void* d_ptr);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RAPIDGNN_B200_H */

@@ -1,0 +1,104 @@
+// C-ABI plumbing: error strings, device probe, CUDA IPC for peer shards.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "rg_common.cuh"
+
+namespace rg {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return RG_ERR_CUDA;
+  }
+  return RG_OK;
+}
+
+__global__ void probe_kernel(int* out) { *out = 100; }
+
+}  // namespace rg
+
+extern "C" const char* rg_last_error(void) { return rg::g_err; }
+
+extern "C" int rg_abi_version(void) { return 1; }
+
+extern "C" int rg_device_ok(void) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) return 0;
+  if (prop.major != 10 || prop.minor != 0) {
+    rg::set_error("device is sm_%d%d; this library is built for sm_100a only", prop.major,
+                  prop.minor);
+    return 0;
+  }
+  int* d = nullptr;
+  int h = 0;
+  if (cudaMalloc(&d, sizeof(int)) != cudaSuccess) return 0;
+  rg::probe_kernel<<<1, 1>>>(d);
+  bool ok = cudaMemcpy(&h, d, sizeof(int), cudaMemcpyDeviceToHost) == cudaSuccess && h == 100;
+  cudaFree(d);
+  if (!ok) rg::set_error("probe kernel failed: %s", cudaGetErrorString(cudaGetLastError()));
+  return ok ? 1 : 0;
+}
+
+// cuMemGetAddressRange through the runtime's driver entry point, so the
+// library does not link libcuda (it must load on GPU-less hosts).
+typedef int (*GetRangeFn)(unsigned long long*, size_t*, unsigned long long);
+
+extern "C" int rg_ipc_handle(const void* d_ptr, uint8_t* h_handle64, int64_t* offset) {
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void*>(d_ptr));
+  if (e != cudaSuccess) {
+    rg::set_error("cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+    return RG_ERR_CUDA;
+  }
+  static_assert(sizeof(h) == 64, "IPC handle size");
+  std::memcpy(h_handle64, &h, 64);
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  e = cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q);
+  if (e != cudaSuccess || fn == nullptr) {
+    rg::set_error("cuMemGetAddressRange unavailable");
+    return RG_ERR_CUDA;
+  }
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (reinterpret_cast<GetRangeFn>(fn)(&base, &size, (unsigned long long)d_ptr) != 0) {
+    rg::set_error("cuMemGetAddressRange failed");
+    return RG_ERR_CUDA;
+  }
+  *offset = (int64_t)((unsigned long long)d_ptr - base);
+  return RG_OK;
+}
+
+extern "C" int rg_ipc_open(const uint8_t* h_handle64, void** d_ptr_out) {
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, h_handle64, 64);
+  cudaError_t e = cudaIpcOpenMemHandle(d_ptr_out, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) {
+    rg::set_error("cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+    return RG_ERR_CUDA;
+  }
+  return RG_OK;
+}
+
+extern "C" int rg_ipc_close(void* d_ptr) {
+  cudaError_t e = cudaIpcCloseMemHandle(d_ptr);
+  if (e != cudaSuccess) {
+    rg::set_error("cudaIpcCloseMemHandle: %s", cudaGetErrorString(e));
+    return RG_ERR_CUDA;
+  }
+  return RG_OK;
+}

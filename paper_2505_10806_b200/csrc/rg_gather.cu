@@ -1,0 +1,179 @@
+// K6/K7: feature-bundle gather, cache fill and pull routing.
+//
+// Reference: gnnpipe/prefetch.py:41-88 (assemble_bundle), cache.py:54-78
+// (FeatureCache.lookup), store.py:66-69 (rows_for_local) and
+// store.py:173-196 (StoreClient._pull).  The reference splits a request
+// into local / cache-hit / fallback ids with searchsorted passes and pulls
+// fallback rows per owner through a byte codec.  Here every node carries one
+// 32-bit route word (owner or cache kind + row index); a warp
+// copies 32 consecutive bundle rows at a time: one coalesced id load, one
+// route load per row, then the rows' 16-byte vectors are streamed with all
+// 32 lanes busy (flattened row x vector index) and written back contiguously.
+// Source rows may live in this GPU's HBM or in a peer GPU's shard (NVLink
+// P2P pointer); the kernel does not distinguish.
+#include "rg_common.cuh"
+
+namespace rg {
+namespace {
+
+constexpr int kGatherWarps = 8;
+constexpr int kUnroll = 8;
+
+struct Bases {
+  const float* p[16];
+};
+
+__global__ void __launch_bounds__(kGatherWarps * 32)
+    gather_bundle_kernel(const int32_t* __restrict__ ids, const int32_t* __restrict__ nids,
+                         int64_t cap, const uint32_t* __restrict__ route, const __grid_constant__ Bases bases,
+                         int stride, int nvec, int dq, int dr, int my_part,
+                         float* __restrict__ out, uint32_t* __restrict__ counters) {
+  __shared__ uint32_t s_cnt[RG_NCOUNTERS];
+  __shared__ const float* s_base[16];
+  const int b = blockIdx.y;
+  const int lane = lane_id();
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x < RG_NCOUNTERS) s_cnt[threadIdx.x] = 0;
+  if (threadIdx.x < 16) s_base[threadIdx.x] = bases.p[threadIdx.x];
+  __syncthreads();
+  const int nrows = nids[b];
+  uint32_t c_local = 0, c_hit = 0, c_fb = 0, c_bad = 0, omask = 0;
+  const int64_t warp_stride = (int64_t)gridDim.x * kGatherWarps * 32;
+  for (int64_t r0 = ((int64_t)blockIdx.x * kGatherWarps + warp) * 32; r0 < nrows;
+       r0 += warp_stride) {
+    const int64_t row = r0 + lane;
+    const bool valid = row < nrows;
+    const int nr = (int)(nrows - r0 < 32 ? nrows - r0 : 32);
+    uint32_t rt = RG_ROUTE_INVALID;
+    if (valid) rt = __ldg(route + __ldg(ids + (int64_t)b * cap + row));
+    const int kind = (int)(rt >> RG_KIND_SHIFT);
+    const float* bp = (valid && rt != RG_ROUTE_INVALID) ? s_base[kind] : nullptr;
+    const bool bad = valid && bp == nullptr;
+    const bool local = valid && !bad && kind == my_part;
+    const bool hit = valid && !bad && kind == (int)RG_KIND_CACHE;
+    const bool fb = valid && !bad && !local && !hit;
+    c_local += __popc(__ballot_sync(kFull, local));
+    c_hit += __popc(__ballot_sync(kFull, hit));
+    c_fb += __popc(__ballot_sync(kFull, fb));
+    c_bad += __popc(__ballot_sync(kFull, bad));
+    omask |= __reduce_or_sync(kFull, fb ? (1u << kind) : 0u);
+    const float* src = nullptr;
+    if (bp) src = bp + (int64_t)(rt & RG_ROW_MASK) * stride;
+    const unsigned long long srcu = reinterpret_cast<unsigned long long>(src);
+    float4* dst = reinterpret_cast<float4*>(out + ((int64_t)b * cap + r0) * stride);
+    const int total = nr * nvec;
+    // lane handles flattened vectors e = lane, lane+32, ...: row e/nvec, col e%nvec
+    int er = lane / nvec, ec = lane - (lane / nvec) * nvec;
+    for (int e0 = 0; e0 < total; e0 += 32 * kUnroll) {
+      float4 v[kUnroll];
+      int rr[kUnroll], cc[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        rr[u] = er;
+        cc[u] = ec;
+        ec += dr;
+        er += dq;
+        if (ec >= nvec) {
+          ec -= nvec;
+          ++er;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const unsigned long long sp = __shfl_sync(kFull, srcu, rr[u] & 31);
+        const int e = e0 + u * 32 + lane;
+        if (e < total && sp)
+          v[u] = ld_stream(reinterpret_cast<const float4*>(sp) + cc[u]);
+        else
+          v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int e = e0 + u * 32 + lane;
+        if (e < total) st_stream(dst + e, v[u]);
+      }
+    }
+  }
+  if (lane == 0) {
+    atomicAdd(&s_cnt[RG_CNT_LOCAL], c_local);
+    atomicAdd(&s_cnt[RG_CNT_HIT], c_hit);
+    atomicAdd(&s_cnt[RG_CNT_FALLBACK], c_fb);
+    atomicAdd(&s_cnt[RG_CNT_BAD], c_bad);
+    atomicOr(&s_cnt[RG_CNT_OWNER_MASK], omask);
+  }
+  __syncthreads();
+  if (threadIdx.x < RG_NCOUNTERS) {
+    const uint32_t x = s_cnt[threadIdx.x];
+    if (x) {
+      uint32_t* g = counters + (int64_t)b * RG_NCOUNTERS + threadIdx.x;
+      if (threadIdx.x == RG_CNT_OWNER_MASK)
+        atomicOr(g, x);
+      else
+        atomicAdd(g, x);
+    }
+  }
+}
+
+__global__ void route_copy_kernel(const uint32_t* __restrict__ base, int64_t n,
+                                  uint32_t* __restrict__ route) {
+  const int64_t n4 = n / 4;
+  const uint4* b4 = reinterpret_cast<const uint4*>(base);
+  uint4* r4 = reinterpret_cast<uint4*>(route);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x)
+    r4[i] = b4[i];
+  for (int64_t i = n4 * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    route[i] = base[i];
+}
+
+__global__ void route_scatter_kernel(const int32_t* __restrict__ hot, int64_t n_hot,
+                                     uint32_t* __restrict__ route) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_hot;
+       i += (int64_t)gridDim.x * blockDim.x)
+    route[hot[i]] = (RG_KIND_CACHE << RG_KIND_SHIFT) | (uint32_t)i;
+}
+
+}  // namespace
+}  // namespace rg
+
+using namespace rg;
+
+extern "C" int rg_gather_bundle(const int32_t* d_ids, const int32_t* d_nids, int64_t cap,
+                                int32_t G, const uint32_t* d_route, const float* const* h_bases,
+                                int32_t stride, int32_t my_part, float* d_out,
+                                uint32_t* d_counters, void* stream) {
+  RG_REQUIRE(G >= 1 && G <= 65535 && cap >= 1, "rg_gather_bundle: bad sizes");
+  RG_REQUIRE(stride >= 4 && stride % 4 == 0, "rg_gather_bundle: stride %d not a multiple of 4",
+             stride);
+  RG_REQUIRE(((uintptr_t)d_out & 15) == 0, "rg_gather_bundle: output not 16-byte aligned");
+  Bases bases;
+  for (int i = 0; i < 16; ++i) {
+    bases.p[i] = h_bases[i];
+    RG_REQUIRE(((uintptr_t)bases.p[i] & 15) == 0, "rg_gather_bundle: base %d misaligned", i);
+  }
+  const int nvec = stride / 4;
+  const int dq = 32 / nvec, dr = 32 % nvec;
+  // enough CTAs for ~4 resident per SM on the largest slot; extra CTAs of a
+  // short batch exit after one bounds check.
+  const int64_t want = (cap + kGatherWarps * 32 - 1) / (kGatherWarps * 32);
+  const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(want, (kNumSMs * 8 + G - 1) / G));
+  gather_bundle_kernel<<<dim3(gx, G), kGatherWarps * 32, 0, (cudaStream_t)stream>>>(
+      d_ids, d_nids, cap, d_route, bases, stride, nvec, dq, dr, my_part, d_out, d_counters);
+  return check_launch("gather_bundle");
+}
+
+extern "C" int rg_route_with_cache(const uint32_t* d_base_route, int64_t n, const int32_t* d_hot,
+                                   int64_t n_hot, uint32_t* d_route, void* stream) {
+  RG_REQUIRE(n >= 1 && n_hot >= 0, "rg_route_with_cache: bad sizes");
+  RG_REQUIRE(n_hot <= (int64_t)RG_ROW_MASK, "rg_route_with_cache: n_hot too large");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (d_route != d_base_route) {
+    route_copy_kernel<<<kNumSMs * 4, 256, 0, s>>>(d_base_route, n, d_route);
+    int rc = check_launch("route_copy");
+    if (rc) return rc;
+  }
+  if (n_hot == 0) return RG_OK;
+  route_scatter_kernel<<<kNumSMs * 2, 256, 0, s>>>(d_hot, n_hot, d_route);
+  return check_launch("route_scatter");
+}

@@ -1,0 +1,471 @@
+// K2/K3: multi-hop neighbour sampling for G mini-batches at once.
+//
+// Reference: gnnpipe/sampler.py:86-152 (_sample_neighbors, sample_block).
+// For frontier node v with degree D at expansion step d the reference keys
+// every position p < D with mix64(nk_v + (p+1)*GOLDEN), nk_v =
+// mix64((v+1)*GOLDEN ^ s_d), and keeps the take = min(D, F) smallest
+// (sampler.py:102-113).  Keys are pairwise distinct inside a node (mix64 is
+// a bijection and GOLDEN is odd) so the selected set is unique and this
+// device version is bit-exact.
+//
+// Layout: one warp per frontier node; the selected neighbour
+// ids are emitted ascending into a fixed-stride ELL row (stride = fanout)
+// with a per-row count, which is exactly the (dst, src)-sorted edge list of
+// sampler.py:145-146 with the dst implied by the row.  The new frontier
+// F_{d+1} = F_d U src (np.union1d, sampler.py:148) is a per-batch bitmap
+// over all n nodes that accumulates across steps; rg_bitmap_compact turns it
+// into the sorted-unique id list.
+#include <climits>
+
+#include "rg_common.cuh"
+
+namespace rg {
+namespace {
+
+constexpr int kSampleWarps = 8;           // 256-thread CTAs
+constexpr int kSlowCap = 4096;            // largest take handled (fanout cap)
+constexpr int kCompactWords = 1024;       // bitmap words per compaction CTA
+constexpr int kCompactThreads = 256;
+constexpr int kScanElems = 1024;          // elements per ELL-scan CTA
+
+__device__ __forceinline__ void mark(uint32_t* bm, int32_t v) {
+  atomicOr(bm + (v >> 5), 1u << (v & 31));
+}
+
+// Selection for D > F, F <= 32: lanes 0..T-1 end up holding the positions of
+// the T smallest keys.  Chunk 0 is bitonic-sorted; later chunks only touch
+// the list when a key beats the current T-th smallest (ballot filter), which
+// for uniform keys happens ~T*ln(D/32) times in total.
+__device__ __forceinline__ int select_positions(uint64_t nk, int D, int T) {
+  const int lane = lane_id();
+  uint64_t kk = nk + (uint64_t)(lane + 1) * GOLDEN;
+  uint64_t key = lane < D ? mix64(kk) : ~0ull;
+  int pos = lane;
+  warp_bitonic_sort(key, pos);
+  uint64_t thr = __shfl_sync(kFull, key, T - 1);
+  const uint64_t step = 32ull * GOLDEN;
+  for (int base = 32; base < D; base += 32) {
+    kk += step;
+    const bool valid = base + lane < D;
+    const uint64_t k2 = mix64(kk);
+    unsigned m = __ballot_sync(kFull, valid && k2 < thr);
+    while (m) {
+      const int s = __ffs(m) - 1;
+      m &= m - 1;
+      const uint64_t ck = __shfl_sync(kFull, k2, s);
+      if (ck < thr) {
+        const int i = __popc(__ballot_sync(kFull, key < ck));
+        const uint64_t uk = __shfl_up_sync(kFull, key, 1);
+        const int up = __shfl_up_sync(kFull, pos, 1);
+        if (lane > i) {
+          key = uk;
+          pos = up;
+        }
+        if (lane == i) {
+          key = ck;
+          pos = base + s;
+        }
+        thr = __shfl_sync(kFull, key, T - 1);
+      }
+    }
+  }
+  return pos;
+}
+
+__global__ void __launch_bounds__(kSampleWarps * 32)
+    sample_level_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                        int G, const int32_t* __restrict__ front, int64_t cap_in,
+                        const int32_t* __restrict__ nfront, int F, uint64_t level_mix,
+                        const uint64_t* __restrict__ rng_seed, int32_t* __restrict__ ell,
+                        int32_t* __restrict__ cnt, uint32_t* __restrict__ bm, int64_t nwords,
+                        int32_t* __restrict__ slow) {
+  __shared__ int s_next;
+  const int lane = lane_id();
+  int maxf = 0;
+  for (int b = lane; b < G; b += 32) maxf = max(maxf, nfront[b]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) maxf = max(maxf, __shfl_xor_sync(kFull, maxf, o));
+  if (threadIdx.x == 0) s_next = 0;
+  __syncthreads();
+  // items k = j*G + b, interleaved so the low (hub-heavy) frontier ranks of
+  // every batch are spread over all CTAs; CTA c owns k = c, c + grid, ...
+  // and its warps pull them dynamically through a shared counter.
+  const int64_t total = (int64_t)maxf * G;
+  const int64_t grid = gridDim.x;
+  for (;;) {
+    int t = 0;
+    if (lane == 0) t = atomicAdd(&s_next, 1);
+    t = __shfl_sync(kFull, t, 0);
+    const int64_t k = blockIdx.x + (int64_t)t * grid;
+    if (k >= total) break;
+    const int j = (int)(k / G), b = (int)(k - (int64_t)j * G);
+    if (j >= nfront[b]) continue;
+    const int64_t row = (int64_t)b * cap_in + j;
+    const int32_t v = front[row];
+    const int64_t a = indptr[v];
+    const int D = (int)(indptr[v + 1] - a);
+    const int T = min(D, F);
+    if (lane == 0) cnt[row] = T;
+    if (T > 32) {  // only reachable with fanout > 32: block path below
+      if (lane == 0) {
+        int at = atomicAdd(slow, 1);
+        slow[1 + at] = (int)k;
+      }
+      continue;
+    }
+    int32_t nb = INT_MAX;
+    if (D <= F) {
+      if (lane < D) nb = __ldg(indices + a + lane);
+    } else {
+      const uint64_t sd = mix64(rng_seed[b] ^ level_mix);
+      const uint64_t nk = mix64(((uint64_t)v + 1ull) * GOLDEN ^ sd);
+      const int pos = select_positions(nk, D, T);
+      if (lane < T) nb = __ldg(indices + a + pos);
+    }
+    warp_bitonic_sort_keys(nb);
+    if (lane < T) {
+      ell[row * F + lane] = nb;
+      mark(bm + (int64_t)b * nwords, nb);
+    }
+  }
+}
+
+// ---- take > 32 (fanout > 32): one CTA per node, shared-memory sort -------
+__device__ void block_sort_smem(int32_t* s, int n) {
+  int P = 1;
+  while (P < n) P <<= 1;
+  for (int i = n + threadIdx.x; i < P; i += blockDim.x) s[i] = INT_MAX;
+  __syncthreads();
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const int l = i ^ j;
+        if (l > i) {
+          const bool up = (i & k) == 0;
+          const int32_t x = s[i], y = s[l];
+          if ((x > y) == up) {
+            s[i] = y;
+            s[l] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    sample_slow_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                       int G, const int32_t* __restrict__ front, int64_t cap_in, int F,
+                       uint64_t level_mix, const uint64_t* __restrict__ rng_seed,
+                       int32_t* __restrict__ ell, uint32_t* __restrict__ bm, int64_t nwords,
+                       const int32_t* __restrict__ slow) {
+  __shared__ int32_t s_val[2 * kSlowCap];
+  __shared__ uint32_t s_hist[256];
+  __shared__ uint64_t s_prefix;
+  __shared__ int s_rank, s_fill;
+  const int nslow = slow[0];
+  for (int it = blockIdx.x; it < nslow; it += gridDim.x) {
+    const int64_t k = slow[1 + it];
+    const int j = (int)(k / G), b = (int)(k - (int64_t)j * G);
+    const int64_t row = (int64_t)b * cap_in + j;
+    const int32_t v = front[row];
+    const int64_t a = indptr[v];
+    const int D = (int)(indptr[v + 1] - a);
+    const int T = min(D, F);
+    if (D <= F) {
+      for (int p = threadIdx.x; p < D; p += blockDim.x) s_val[p] = indices[a + p];
+    } else {
+      // radix-select the T-th smallest key (8 passes of 8 bits), then keep
+      // every position whose key is <= it: exactly T positions.
+      const uint64_t sd = mix64(rng_seed[b] ^ level_mix);
+      const uint64_t nk = mix64(((uint64_t)v + 1ull) * GOLDEN ^ sd);
+      if (threadIdx.x == 0) {
+        s_prefix = 0;
+        s_rank = T;  // 1-based rank still to find inside the prefix class
+        s_fill = 0;
+      }
+      for (int shift = 56; shift >= 0; shift -= 8) {
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) s_hist[i] = 0;
+        __syncthreads();
+        const uint64_t hi_mask = shift == 56 ? 0ull : (~0ull << (shift + 8));
+        const uint64_t prefix = s_prefix;
+        for (int p = threadIdx.x; p < D; p += blockDim.x) {
+          const uint64_t key = mix64(nk + (uint64_t)(p + 1) * GOLDEN);
+          if ((key & hi_mask) == prefix) atomicAdd(&s_hist[(key >> shift) & 255], 1u);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          int r = s_rank;
+          int dgt = 0;
+          while ((int)s_hist[dgt] < r) r -= s_hist[dgt++];
+          s_rank = r;
+          s_prefix = prefix | ((uint64_t)dgt << shift);
+        }
+        __syncthreads();
+      }
+      const uint64_t kth = s_prefix;
+      for (int p = threadIdx.x; p < D; p += blockDim.x) {
+        const uint64_t key = mix64(nk + (uint64_t)(p + 1) * GOLDEN);
+        if (key <= kth) s_val[atomicAdd(&s_fill, 1)] = indices[a + p];
+      }
+    }
+    __syncthreads();
+    block_sort_smem(s_val, T);
+    int32_t* out = ell + row * F;
+    uint32_t* bmb = bm + (int64_t)b * nwords;
+    for (int i = threadIdx.x; i < T; i += blockDim.x) {
+      out[i] = s_val[i];
+      mark(bmb, s_val[i]);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void mark_seeds_kernel(const int32_t* __restrict__ seeds,
+                                  const int32_t* __restrict__ nseeds, int seed_cap,
+                                  uint32_t* __restrict__ bm, int64_t nwords) {
+  const int b = blockIdx.y;
+  const int ns = nseeds[b];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ns; i += gridDim.x * blockDim.x)
+    mark(bm + (int64_t)b * nwords, seeds[(int64_t)b * seed_cap + i]);
+}
+
+// ---- bitmap -> sorted unique ids ----------------------------------------
+__global__ void __launch_bounds__(kCompactThreads)
+    bitmap_count_kernel(const uint32_t* __restrict__ bm, int64_t nwords, int64_t nchunks,
+                        int32_t* __restrict__ chunk_tot) {
+  __shared__ int s_red[32];
+  const int b = blockIdx.y;
+  const uint32_t* w = bm + (int64_t)b * nwords;
+  const int64_t w0 = (int64_t)blockIdx.x * kCompactWords + threadIdx.x * 4;
+  int c = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (w0 + i < nwords) c += __popc(w[w0 + i]);
+  int tot;
+  block_excl_scan<kCompactThreads>(c, s_red, &tot);
+  if (threadIdx.x == 0) chunk_tot[(int64_t)b * nchunks + blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kCompactThreads)
+    bitmap_emit_kernel(const uint32_t* __restrict__ bm, int64_t nwords, int64_t nchunks,
+                       const int32_t* __restrict__ chunk_tot, int32_t* __restrict__ out,
+                       int64_t cap_out, int32_t* __restrict__ nout, int32_t* __restrict__ wpre) {
+  __shared__ int s_red[32];
+  __shared__ int s_base;
+  const int b = blockIdx.y;
+  const int64_t chunk = blockIdx.x;
+  // base = sum of the preceding chunk totals (and the grand total for CTA 0)
+  int before = 0, all = 0;
+  for (int64_t c = threadIdx.x; c < nchunks; c += blockDim.x) {
+    const int t = chunk_tot[(int64_t)b * nchunks + c];
+    all += t;
+    if (c < chunk) before += t;
+  }
+  int tot;
+  block_excl_scan<kCompactThreads>(before, s_red, &tot);
+  if (threadIdx.x == 0) s_base = tot;
+  __syncthreads();
+  const int base = s_base;
+  __syncthreads();
+  if (chunk == 0) {
+    int grand;
+    block_excl_scan<kCompactThreads>(all, s_red, &grand);
+    if (threadIdx.x == 0) nout[b] = grand;
+  }
+  const uint32_t* w = bm + (int64_t)b * nwords;
+  const int64_t w0 = chunk * kCompactWords + threadIdx.x * 4;
+  uint32_t words[4];
+  int c = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    words[i] = (w0 + i < nwords) ? w[w0 + i] : 0u;
+    c += __popc(words[i]);
+  }
+  int dummy;
+  int at = base + block_excl_scan<kCompactThreads>(c, s_red, &dummy);
+  int32_t* o = out + (int64_t)b * cap_out;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (w0 + i >= nwords) break;
+    if (wpre) wpre[(int64_t)b * nwords + w0 + i] = at;
+    uint32_t m = words[i];
+    const int32_t id0 = (int32_t)((w0 + i) * 32);
+    while (m) {
+      const int bit = __ffs(m) - 1;
+      m &= m - 1;
+      if (at < cap_out) o[at] = id0 + bit;
+      ++at;
+    }
+  }
+}
+
+__global__ void bitmap_set_kernel(const int32_t* __restrict__ ids, const int32_t* __restrict__ n,
+                                  uint32_t* __restrict__ bm) {
+  const int cnt = *n;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x)
+    mark(bm, ids[i]);
+}
+
+// ---- ELL -> flat (src, dst) edges for the numpy API ----------------------
+__global__ void __launch_bounds__(256)
+    ell_count_kernel(const int32_t* __restrict__ nfront, int64_t cap_in,
+                     const int32_t* __restrict__ cnt, int64_t nchunks,
+                     int32_t* __restrict__ chunk_tot) {
+  __shared__ int s_red[32];
+  const int b = blockIdx.y;
+  const int nf = nfront[b];
+  const int64_t j0 = (int64_t)blockIdx.x * kScanElems + threadIdx.x * 4;
+  int c = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (j0 + i < nf) c += cnt[(int64_t)b * cap_in + j0 + i];
+  int tot;
+  block_excl_scan<256>(c, s_red, &tot);
+  if (threadIdx.x == 0) chunk_tot[(int64_t)b * nchunks + blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(256)
+    ell_emit_kernel(const int32_t* __restrict__ front, const int32_t* __restrict__ nfront,
+                    int64_t cap_in, const int32_t* __restrict__ ell,
+                    const int32_t* __restrict__ cnt, int F, int64_t nchunks,
+                    const int32_t* __restrict__ chunk_tot, int32_t* __restrict__ eoff,
+                    int32_t* __restrict__ src, int32_t* __restrict__ dst, int64_t cap_e,
+                    int32_t* __restrict__ nedge) {
+  __shared__ int s_red[32];
+  __shared__ int s_base;
+  const int b = blockIdx.y;
+  const int nf = nfront[b];
+  const int64_t chunk = blockIdx.x;
+  int before = 0, all = 0;
+  for (int64_t c = threadIdx.x; c < nchunks; c += blockDim.x) {
+    const int t = chunk_tot[(int64_t)b * nchunks + c];
+    all += t;
+    if (c < chunk) before += t;
+  }
+  int tot;
+  block_excl_scan<256>(before, s_red, &tot);
+  if (threadIdx.x == 0) s_base = tot;
+  __syncthreads();
+  const int base = s_base;
+  __syncthreads();
+  int grand;
+  block_excl_scan<256>(all, s_red, &grand);
+  if (chunk == 0 && threadIdx.x == 0) {
+    nedge[b] = grand;
+    eoff[(int64_t)b * (cap_in + 1) + nf] = grand;
+  }
+  const int64_t j0 = chunk * kScanElems + threadIdx.x * 4;
+  int c[4];
+  int sum = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    c[i] = (j0 + i < nf) ? cnt[(int64_t)b * cap_in + j0 + i] : 0;
+    sum += c[i];
+  }
+  int dummy;
+  int at = base + block_excl_scan<256>(sum, s_red, &dummy);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t j = j0 + i;
+    if (j >= nf) break;
+    const int64_t row = (int64_t)b * cap_in + j;
+    eoff[(int64_t)b * (cap_in + 1) + j] = at;
+    const int32_t d = front[row];
+    for (int r = 0; r < c[i]; ++r) {
+      if (at < cap_e) {
+        src[(int64_t)b * cap_e + at] = ell[row * F + r];
+        dst[(int64_t)b * cap_e + at] = d;
+      }
+      ++at;
+    }
+  }
+}
+
+}  // namespace
+}  // namespace rg
+
+using namespace rg;
+
+extern "C" int rg_mark_seeds(const int32_t* d_seeds, const int32_t* d_nseeds, int32_t G,
+                             int32_t seed_cap, uint32_t* d_bm, int64_t nwords, void* stream) {
+  RG_REQUIRE(G >= 1 && G <= 65535 && seed_cap >= 1, "rg_mark_seeds: bad G=%d cap=%d", G,
+             seed_cap);
+  const int blocks = (int)std::min<int64_t>((seed_cap + 255) / 256, 64);
+  mark_seeds_kernel<<<dim3(blocks, G), 256, 0, (cudaStream_t)stream>>>(d_seeds, d_nseeds,
+                                                                       seed_cap, d_bm, nwords);
+  return check_launch("mark_seeds");
+}
+
+extern "C" int rg_sample_level(const int64_t* d_indptr, const int32_t* d_indices, int64_t n,
+                               int32_t G, const int32_t* d_front, int64_t cap_in,
+                               const int32_t* d_nfront, int32_t fanout, int32_t level,
+                               const uint64_t* d_rng_seed, int32_t* d_ell, int32_t* d_cnt,
+                               uint32_t* d_bm, int64_t nwords, int32_t* d_slow, void* stream) {
+  RG_REQUIRE(G >= 1 && cap_in >= 1 && n >= 1, "rg_sample_level: bad sizes");
+  RG_REQUIRE(fanout >= 1, "rg_sample_level: fanout must be >= 1");
+  if (fanout > kSlowCap) {
+    set_error("rg_sample_level: fanout %d above the supported %d", fanout, kSlowCap);
+    return RG_ERR_UNSUPPORTED;
+  }
+  RG_REQUIRE(fanout <= 32 || d_slow != nullptr, "rg_sample_level: fanout > 32 needs d_slow");
+  cudaStream_t s = (cudaStream_t)stream;
+  const uint64_t level_mix = (uint64_t)(level + 1) * GOLDEN;  // sampler.py:143
+  int32_t* slow = fanout > 32 ? d_slow : nullptr;
+  if (slow && cudaMemsetAsync(slow, 0, sizeof(int32_t), s) != cudaSuccess)
+    return check_launch("sample_level memset");
+  const int grid = kNumSMs * 4;
+  sample_level_kernel<<<grid, kSampleWarps * 32, 0, s>>>(d_indptr, d_indices, G, d_front, cap_in,
+                                                         d_nfront, fanout, level_mix, d_rng_seed,
+                                                         d_ell, d_cnt, d_bm, nwords, slow);
+  int rc = check_launch("sample_level");
+  if (rc || !slow) return rc;
+  sample_slow_kernel<<<kNumSMs, 256, 0, s>>>(d_indptr, d_indices, G, d_front, cap_in, fanout,
+                                             level_mix, d_rng_seed, d_ell, d_bm, nwords, slow);
+  return check_launch("sample_slow");
+}
+
+extern "C" int64_t rg_bitmap_chunks(int64_t nwords) {
+  return (nwords + kCompactWords - 1) / kCompactWords;
+}
+
+extern "C" int rg_bitmap_compact(const uint32_t* d_bm, int64_t nwords, int32_t G,
+                                 int32_t* d_chunk, int32_t* d_out, int64_t cap_out,
+                                 int32_t* d_nout, int32_t* d_wpre, void* stream) {
+  RG_REQUIRE(G >= 1 && G <= 65535 && nwords >= 1, "rg_bitmap_compact: bad sizes");
+  const int64_t nchunks = rg_bitmap_chunks(nwords);
+  RG_REQUIRE(nchunks < (1ll << 31), "rg_bitmap_compact: too many chunks");
+  cudaStream_t s = (cudaStream_t)stream;
+  dim3 grid((unsigned)nchunks, G);
+  bitmap_count_kernel<<<grid, kCompactThreads, 0, s>>>(d_bm, nwords, nchunks, d_chunk);
+  int rc = check_launch("bitmap_count");
+  if (rc) return rc;
+  bitmap_emit_kernel<<<grid, kCompactThreads, 0, s>>>(d_bm, nwords, nchunks, d_chunk, d_out,
+                                                      cap_out, d_nout, d_wpre);
+  return check_launch("bitmap_emit");
+}
+
+extern "C" int rg_bitmap_set(const int32_t* d_ids, const int32_t* d_n, uint32_t* d_bm,
+                             void* stream) {
+  bitmap_set_kernel<<<kNumSMs * 2, 256, 0, (cudaStream_t)stream>>>(d_ids, d_n, d_bm);
+  return check_launch("bitmap_set");
+}
+
+extern "C" int64_t rg_scan_chunks(int64_t cap) { return (cap + kScanElems - 1) / kScanElems; }
+
+extern "C" int rg_ell_to_edges(const int32_t* d_front, const int32_t* d_nfront, int64_t cap_in,
+                               const int32_t* d_ell, const int32_t* d_cnt, int32_t fanout,
+                               int32_t G, int32_t* d_chunk, int32_t* d_eoff, int32_t* d_src,
+                               int32_t* d_dst, int64_t cap_e, int32_t* d_nedge, void* stream) {
+  RG_REQUIRE(G >= 1 && G <= 65535 && cap_in >= 1 && fanout >= 1, "rg_ell_to_edges: bad sizes");
+  const int64_t nchunks = rg_scan_chunks(cap_in);
+  cudaStream_t s = (cudaStream_t)stream;
+  dim3 grid((unsigned)nchunks, G);
+  ell_count_kernel<<<grid, 256, 0, s>>>(d_nfront, cap_in, d_cnt, nchunks, d_chunk);
+  int rc = check_launch("ell_count");
+  if (rc) return rc;
+  ell_emit_kernel<<<grid, 256, 0, s>>>(d_front, d_nfront, cap_in, d_ell, d_cnt, fanout, nchunks,
+                                       d_chunk, d_eoff, d_src, d_dst, cap_e, d_nedge);
+  return check_launch("ell_emit");
+}

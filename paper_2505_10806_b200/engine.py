@@ -1,0 +1,242 @@
+"""Device engine: HBM-resident graph, group sampler, feature store, gather.
+
+Everything here is plumbing around the C ABI (include/rapidgnn_b200.h):
+torch provides device memory and the current CUDA stream, every compute
+step is one of the library's sm_100a kernels.  All work of one call is
+enqueued on torch's current stream without host synchronisation, so a
+whole group (sample L levels + gather) can be captured in a CUDA graph.
+
+Data layout:
+  indptr   int64[n+1]        indices int32[E]
+  owner    uint8[n]          route   uint32[n] = owner<<28 | row in shard
+  shard q  float32[n_q, stride]  (stride = feat_dim rounded up to 4)
+  cache    float32[n_hot, stride]; cache route = route with hot ids
+           rewritten to (15<<28 | slot)
+  group buffers: G slots per level; slot b of level d at b*cap_d.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import ptr
+
+I32 = torch.int32
+
+
+def stride_for(d: int) -> int:
+    return max(4, (d + 3) // 4 * 4)
+
+
+def _cur() -> int:
+    return _lib.stream_handle()
+
+
+class DeviceGraph:
+    """CSR graph in HBM: indptr int64, indices int32 (ids < 2^31)."""
+
+    def __init__(self, indptr: np.ndarray, indices: np.ndarray, num_nodes: int, device=None):
+        _lib.device()
+        if num_nodes >= 2**31 - 1:
+            raise NotImplementedError("node ids must fit in int32")
+        self.device = torch.device(device or "cuda")
+        self.n = int(num_nodes)
+        self.nwords = (self.n + 31) // 32
+        self.indptr = torch.from_numpy(np.ascontiguousarray(indptr, dtype=np.int64)).to(self.device)
+        self.indices = torch.from_numpy(np.ascontiguousarray(indices, dtype=np.int32)).to(self.device)
+        self.num_edges = int(self.indices.numel())
+
+    @classmethod
+    def of(cls, g) -> "DeviceGraph":
+        """Device copy of a Graph (ours or the reference's), cached on it."""
+        cached = getattr(g, "_rg_device", None)
+        if cached is not None and cached[0] is g.indptr and cached[1] is g.indices:
+            return cached[2]
+        dg = cls(g.indptr, g.indices, g.num_nodes)
+        try:
+            object.__setattr__(g, "_rg_device", (g.indptr, g.indices, dg))
+        except AttributeError:
+            pass
+        return dg
+
+
+class BlockSampler:
+    """Samples up to G mini-batches per run() (sampler.py:116-152).
+
+    Level d of slot b lives at front[d][b, :nfront[d, b]] (sorted unique
+    ids), its sampled edges as ELL rows ell[d][b, j*F_d : j*F_d+cnt[d][b,j]]
+    (ascending src, dst = front[d][b, j]).  front[L] is the input node set.
+    """
+
+    def __init__(self, dg: DeviceGraph, fanouts, seed_cap: int, group: int = 1):
+        if len(fanouts) == 0:
+            raise ValueError("fanouts must be nonempty")
+        if any(int(f) < 1 for f in fanouts):
+            raise ValueError("fanouts must be >= 1")
+        self.dg = dg
+        self.G = int(group)
+        self.L = len(fanouts)
+        self.fanouts = [int(f) for f in fanouts]
+        self.step_fan = [self.fanouts[self.L - 1 - d] for d in range(self.L)]
+        caps = [int(seed_cap)]
+        for f in self.step_fan:
+            caps.append(min(dg.n, caps[-1] * (1 + f)))
+        self.caps = caps
+        dev, G = dg.device, self.G
+        self.seeds = torch.zeros((G, caps[0]), dtype=I32, device=dev)
+        self.nseeds = torch.zeros(G, dtype=I32, device=dev)
+        self.rng = torch.zeros(G, dtype=torch.int64, device=dev)  # uint64 bits
+        self.front = [torch.empty((G, c), dtype=I32, device=dev) for c in caps]
+        self.nfront = torch.zeros((self.L + 1, G), dtype=I32, device=dev)
+        self.ell = [torch.empty((G, caps[d] * self.step_fan[d]), dtype=I32, device=dev)
+                    for d in range(self.L)]
+        self.cnt = [torch.empty((G, caps[d]), dtype=I32, device=dev) for d in range(self.L)]
+        self.bm = torch.empty((G, dg.nwords), dtype=I32, device=dev)
+        lib = _lib.device()
+        self.chunk = torch.empty((G, int(lib.rg_bitmap_chunks(dg.nwords))), dtype=I32, device=dev)
+        self.slow = (torch.empty(1 + G * max(caps[:-1]), dtype=I32, device=dev)
+                     if max(self.step_fan) > 32 else None)
+
+    def set_seeds(self, b: int, seeds: np.ndarray, rng_seed: int) -> None:
+        """Host seeds for slot b (API path; the plan path fills on device)."""
+        s = torch.from_numpy(np.ascontiguousarray(seeds, dtype=np.int32))
+        self.seeds[b, : len(s)].copy_(s, non_blocking=False)
+        self.nseeds[b] = len(s)
+        self.rng[b] = int(np.uint64(rng_seed & (2**64 - 1)).astype(np.int64))
+
+    def run(self, ngroup: int | None = None) -> None:
+        """Sample all L levels for slots [0, ngroup) on the current stream."""
+        G = self.G if ngroup is None else int(ngroup)
+        dg, s = self.dg, _cur()
+        self.bm[:G].zero_()
+        _lib.call("rg_mark_seeds", ptr(self.seeds), ptr(self.nseeds), G, self.caps[0],
+                  ptr(self.bm), dg.nwords, s)
+        _lib.call("rg_bitmap_compact", ptr(self.bm), dg.nwords, G, ptr(self.chunk),
+                  ptr(self.front[0]), self.caps[0], ptr(self.nfront[0]), None, s)
+        for d in range(self.L):
+            _lib.call("rg_sample_level", ptr(dg.indptr), ptr(dg.indices), dg.n, G,
+                      ptr(self.front[d]), self.caps[d], ptr(self.nfront[d]), self.step_fan[d], d,
+                      ptr(self.rng), ptr(self.ell[d]), ptr(self.cnt[d]), ptr(self.bm), dg.nwords,
+                      ptr(self.slow), s)
+            _lib.call("rg_bitmap_compact", ptr(self.bm), dg.nwords, G, ptr(self.chunk),
+                      ptr(self.front[d + 1]), self.caps[d + 1], ptr(self.nfront[d + 1]), None, s)
+
+    def edges(self, d: int, ngroup: int | None = None):
+        """Flat (src, dst) of level d for every slot: (src, dst, nedge) device."""
+        G = self.G if ngroup is None else int(ngroup)
+        F, cap = self.step_fan[d], self.caps[d]
+        dev = self.dg.device
+        cap_e = cap * F
+        src = torch.empty((G, cap_e), dtype=I32, device=dev)
+        dst = torch.empty((G, cap_e), dtype=I32, device=dev)
+        eoff = torch.empty((G, cap + 1), dtype=I32, device=dev)
+        nedge = torch.empty(G, dtype=I32, device=dev)
+        lib = _lib.device()
+        chunk = torch.empty((G, int(lib.rg_scan_chunks(cap))), dtype=I32, device=dev)
+        _lib.call("rg_ell_to_edges", ptr(self.front[d]), ptr(self.nfront[d]), cap,
+                  ptr(self.ell[d]), ptr(self.cnt[d]), F, G, ptr(chunk), ptr(eoff), ptr(src),
+                  ptr(dst), cap_e, ptr(nedge), _cur())
+        return src, dst, nedge
+
+    def check_caps(self, ngroup: int | None = None) -> None:
+        G = self.G if ngroup is None else int(ngroup)
+        nf = self.nfront[:, :G].cpu()
+        for d in range(self.L + 1):
+            if int(nf[d].max()) > self.caps[d]:
+                raise RuntimeError(f"frontier {d} overflow: {int(nf[d].max())} > {self.caps[d]}")
+
+
+def route_table(owner: np.ndarray, shard_ids: list[np.ndarray | None]) -> np.ndarray:
+    """uint32 route words: owner<<28 | row of v inside its owner's shard.
+    Nodes whose owner shard does not hold them get RG_ROUTE_INVALID
+    (a pull for them is NOT_OWNED, store.py:186-187)."""
+    owner = np.asarray(owner).astype(np.int64)
+    n = len(owner)
+    route = np.full(n, _lib.RG_ROUTE_INVALID, dtype=np.uint32)
+    for q, ids in enumerate(shard_ids):
+        if ids is None or len(ids) == 0:
+            continue
+        ids = np.asarray(ids, dtype=np.int64)
+        if len(ids) > _lib.RG_ROW_MASK:
+            raise NotImplementedError("shard larger than 2^28 rows")
+        mine = ids[(ids >= 0) & (ids < n)]
+        ok = owner[mine] == q
+        rows = np.flatnonzero((ids >= 0) & (ids < n))[ok]
+        route[ids[rows]] = (np.uint32(q) << np.uint32(_lib.RG_KIND_SHIFT)) | rows.astype(np.uint32)
+    return route
+
+
+def as_i32_bits(a: np.ndarray) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int32))
+
+
+class FeatureStore:
+    """All partition shards this GPU can address (local HBM or peer).
+
+    shards[q] is a float32 (n_q, stride) tensor or None; bases[q] its device
+    address (may be an NVLink peer address opened over CUDA IPC)."""
+
+    def __init__(self, owner: np.ndarray, num_parts: int, feat_dim: int, device=None):
+        _lib.device()
+        if num_parts > _lib.RG_MAX_PARTS:
+            raise NotImplementedError(f"at most {_lib.RG_MAX_PARTS} partitions")
+        self.device = torch.device(device or "cuda")
+        self.k = int(num_parts)
+        self.d = int(feat_dim)
+        self.stride = stride_for(self.d)
+        self.owner_np = np.asarray(owner)
+        self.n = len(self.owner_np)
+        self.owner = torch.from_numpy(self.owner_np.astype(np.uint8)).to(self.device)
+        self.shards: list[torch.Tensor | None] = [None] * self.k
+        self.bases = [0] * 16
+        self.route = None
+
+    def set_shard(self, q: int, rows: torch.Tensor | None, base: int | None = None) -> None:
+        self.shards[q] = rows
+        self.bases[q] = int(base if base is not None else (rows.data_ptr() if rows is not None else 0))
+
+    def build_route(self, shard_ids: list[np.ndarray | None]) -> None:
+        self.route = as_i32_bits(route_table(self.owner_np, shard_ids)).to(self.device)
+
+    @staticmethod
+    def pad_rows(rows: np.ndarray, stride: int, device) -> torch.Tensor:
+        rows = np.ascontiguousarray(rows, dtype=np.float32)
+        t = torch.zeros((rows.shape[0], stride), dtype=torch.float32, device=device)
+        if rows.size:
+            t[:, : rows.shape[1]].copy_(torch.from_numpy(rows))
+        return t
+
+
+def bases_array(bases) -> np.ndarray:
+    a = np.zeros(16, dtype=np.uint64)
+    a[: len(bases)] = [int(b) for b in bases]
+    return a
+
+
+def gather_bundle(ids: torch.Tensor, nids: torch.Tensor, cap: int, G: int, route: torch.Tensor,
+                  bases: np.ndarray, stride: int, my_part: int, out: torch.Tensor,
+                  counters: torch.Tensor) -> None:
+    """rg_gather_bundle on the current stream (bases: host uint64[16])."""
+    _lib.call("rg_gather_bundle", ptr(ids), ptr(nids), cap, G, ptr(route), bases.ctypes.data,
+              stride, my_part, ptr(out), ptr(counters), _cur())
+
+
+def gather_rows(base: torch.Tensor, row_idx: np.ndarray | torch.Tensor, stride: int) -> torch.Tensor:
+    """out[i] = base[row_idx[i]] via the bundle kernel with an identity route."""
+    dev = base.device
+    idx = (torch.from_numpy(np.ascontiguousarray(row_idx, dtype=np.int32)).to(dev)
+           if isinstance(row_idx, np.ndarray) else row_idx.to(torch.int32))
+    n = int(idx.numel())
+    out = torch.empty((max(n, 1), stride), dtype=torch.float32, device=dev)
+    if n == 0:
+        return out[:0]
+    # route: kind 0 | row index, ids 0..n-1 index the route directly
+    route = idx  # row index < 2^28, kind bits zero => shard 0
+    ids = torch.arange(n, dtype=I32, device=dev)
+    nids = torch.tensor([n], dtype=I32, device=dev)
+    bases = bases_array([base.data_ptr()])
+    counters = torch.zeros((1, _lib.RG_NCOUNTERS), dtype=I32, device=dev)
+    gather_bundle(ids, nids, n, 1, route, bases, stride, 0, out, counters)
+    return out
