@@ -1,0 +1,473 @@
+#!/usr/bin/env python
+"""bench.py — RapidGNN sample+fetch hot path on B200 (BASELINE.json metric).
+
+A step = one group of G consecutive mini-batches of the plan, each put
+through the reference's per-batch producer body (prefetch.py:123-125:
+plan.block -> sample_block, then assemble_bundle for worker p with the
+epoch's steady hot cache).  value = worker-batches/s summed over GPUs.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+  python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+
+Inputs: gnnpipe.synth_powerlaw(n, m, d, C, seed=7) of the named shape,
+reproduced bit-exactly by the native generator, partitioned with
+partition_edgecut(k).  Rank r runs worker p = r; partition shard q lives on
+GPU q mod N (peer shards read over NVLink through CUDA IPC pointers).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import multiprocessing as mp
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "sample+fetch mini-batches/s, Products-shape, 1-8 B200; remote rows/epoch"
+CONFIGS = {
+    "products": dict(n=2_449_029, m=13, d=100, classes=47, fanouts=[15, 10, 5], batch=1024,
+                     parts=8),
+    "reddit": dict(n=232_965, m=246, d=602, classes=41, fanouts=[25, 10], batch=1024, parts=8),
+    "c1": dict(n=100_000, m=10, d=128, classes=8, fanouts=[10, 5], batch=1024, parts=2),
+}
+S0 = 7
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="products", choices=sorted(CONFIGS))
+    ap.add_argument("--group", type=int, default=8)
+    ap.add_argument("--cache-pct", type=float, default=15.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--nvtx", action="store_true", help="NVTX range 'timed' around the timed steps")
+    return ap.parse_args()
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------- inputs
+def build_inputs(cfg):
+    from paper_2505_10806_b200.graph import synth_powerlaw
+    from paper_2505_10806_b200.partition import partition_edgecut
+
+    t = time.time()
+    g = synth_powerlaw(cfg["n"], cfg["m"], cfg["d"], cfg["classes"], S0)
+    book = partition_edgecut(g, cfg["parts"])
+    log(f"[bench] inputs: n={g.num_nodes} E={g.num_edges} in {time.time() - t:.1f}s")
+    return g, book
+
+
+# ---------------------------------------------------------------- clocks
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                      f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        reasons = sorted({self.NAMES[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(kernel: str):
+    p = ROOT / "profiles" / "traffic.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get(kernel)
+    return None
+
+
+# ---------------------------------------------------------------- CPU oracle (port)
+_CPU = {}
+
+
+def _cpu_init(state):
+    _CPU.update(state)
+
+
+def _cpu_batch(i: int) -> int:
+    """One reference mini-batch on the host: oracle sample_block + bundle
+    rows + provenance accounting (the producer body, prefetch.py:123-125)."""
+    from oracle import gnn_oracle as orc
+
+    st = _CPU
+    seeds = st["perm"][i * st["batch"]:(i + 1) * st["batch"]]
+    fr, _ = orc.block(st["indptr"], st["indices"], seeds, st["fanouts"],
+                      orc.batch_seed(S0, 0, i))
+    ids = fr[-1]
+    rows = st["features"][ids]
+    orc.route_counts(ids, st["owner"], st["part"], st["hot"])
+    return int(rows.shape[0])
+
+
+def cpu_state(g, book, cfg, hot_ids, part=0):
+    from oracle import gnn_oracle as orc
+
+    train = np.flatnonzero(g.train_mask)
+    return {"perm": orc.epoch_order(train, S0, 0), "batch": cfg["batch"], "indptr": g.indptr,
+            "indices": g.indices, "fanouts": cfg["fanouts"], "features": g.features,
+            "owner": book.owner, "part": part, "hot": hot_ids}
+
+
+def cpu_baseline(state, seconds: float, nb: int):
+    """Oracle port timed on the host cores: fork P = cpu_count workers, each
+    takes batches i = r, r+P, ... ; bounded to ~`seconds` of wall time."""
+    _cpu_init(state)
+    t = time.time()
+    _cpu_batch(0)
+    t1 = time.time() - t
+    cores = os.cpu_count() or 1
+    per = max(1, int(seconds / max(t1, 1e-3) / 1.5))
+    total = min(nb, cores * per)
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores, initializer=_cpu_init, initargs=(state,)) as pool:
+        pool.map(_cpu_batch, range(min(cores, total)))  # warm the workers
+        t = time.time()
+        pool.map(_cpu_batch, range(total), chunksize=1)
+        wall = time.time() - t
+    return {"value": total / wall, "unit": "batches/s", "cores": cores, "kind": "port",
+            "sample": f"{total} mini-batches of epoch 0 (oracle sample_block + bundle rows + "
+                      f"accounting, worker 0) over {cores} forked processes; "
+                      f"1-process {1.0 / t1:.3f} batches/s"}
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    g, book = build_inputs(cfg)
+    # uncached baseline mode: every remote row is a fallback pull (the copy
+    # work per batch is the same as with a cache)
+    state = cpu_state(g, book, cfg, np.empty(0, np.int64))
+    _cpu_init(state)
+    cores = os.cpu_count() or 1
+    nb = -(-int(g.train_mask.sum()) // cfg["batch"])
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores, initializer=_cpu_init, initargs=(state,)) as pool:
+        i = 0
+        for _ in range(args.warmup):
+            pool.map(_cpu_batch, [(i + r) % nb for r in range(cores)], chunksize=1)
+            i += cores
+        t = time.time()
+        for _ in range(args.steps):
+            pool.map(_cpu_batch, [(i + r) % nb for r in range(cores)], chunksize=1)
+            i += cores
+        wall = time.time() - t
+    value = args.steps * cores / wall
+    line = {"metric": METRIC, "value": value, "unit": "batches/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic (gnnpipe.synth_powerlaw shape, bit-identical native generator)",
+            "impl": "reference",
+            "config": {"workload": args.config, "batch_size": cfg["batch"],
+                       "fanouts": cfg["fanouts"], "partitions": cfg["parts"],
+                       "batches_per_step": cores, "cache": "none (baseline mode)"},
+            "cpu_baseline": {"value": value, "unit": "batches/s", "cores": cores, "kind": "port",
+                             "sample": f"{args.steps} steps x {cores} mini-batches, oracle port "
+                                       f"of sample_block + assemble_bundle, one per process"},
+            "e2e": {"value": value, "unit": "batches/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- B200 arm
+def main():
+    args = parse()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2505_10806_b200 import _lib
+    from paper_2505_10806_b200.engine import DeviceGraph, FeatureStore
+    from paper_2505_10806_b200.pipeline import WorkerPipeline, resolve_n_hot
+    from paper_2505_10806_b200.plan import candidates, threshold_select
+    from paper_2505_10806_b200.sampler import SeedSchedule
+    from paper_2505_10806_b200 import multigpu
+
+    g, book = build_inputs(cfg)
+    k, d = cfg["parts"], cfg["d"]
+    if world > k:
+        raise SystemExit(f"--gpus {world} > partitions {k}")
+    part = rank
+    owner = book.owner
+    dg = DeviceGraph(g.indptr, g.indices, g.num_nodes)
+    store = FeatureStore(owner, k, d)
+    shard_ids = [np.flatnonzero(owner == q) for q in range(k)]
+    for q in range(k):
+        if q % world == rank:
+            store.set_shard(q, FeatureStore.pad_rows(g.features[shard_ids[q]], store.stride,
+                                                     dg.device))
+    if world > 1:
+        multigpu.exchange_shards(store, rank, world)
+    store.build_route(shard_ids)
+    train = np.flatnonzero(g.train_mask)
+    pipe = WorkerPipeline(dg, store, part, train, cfg["fanouts"], cfg["batch"], S0, args.group)
+    nb, G = pipe.nb, pipe.G
+    sched = SeedSchedule(S0, 1, nb)
+
+    # per-epoch part: plan pass (access counts), hot set, cache fill
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    counts = pipe.count_epoch(sched, 0)
+    ev1.record()
+    torch.cuda.synchronize()
+    plan_ms = ev0.elapsed_time(ev1)
+    _, nout, hist, bm = candidates(counts, store.owner, part, nb)
+    n_remote = int(nout.item())
+    n_hot = resolve_n_hot(args.cache_pct, n_remote)
+    hot = threshold_select(counts, bm, hist.cpu().numpy().astype(np.int64), n_hot)
+    pipe.build_cache(hot)
+    pipe.start_epoch(sched, 0)
+    torch.cuda.synchronize()
+    log(f"[bench] rank {rank}: plan pass {plan_ms:.1f} ms, {n_remote} remote, n_hot {n_hot}")
+
+    n_full = max(1, nb // G)
+    smp = pipe.sampler
+
+    def step(kk, timed_events=None):
+        i0 = (kk % n_full) * G
+        ng = min(G, nb - i0)
+        pipe.plan.fill(pipe.perm, 0, i0, ng)
+        smp.run(ng)
+        if timed_events is not None:
+            timed_events[0].record()
+        pipe.gather(ng, i0)
+        if timed_events is not None:
+            timed_events[1].record()
+        return i0, ng
+
+    for kk in range(args.warmup):
+        step(kk)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    gev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    timed_batches = []
+    launches0 = pipe.launches
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        if args.nvtx:
+            torch.cuda.nvtx.range_push("timed")
+        start.record()
+        for kk in range(args.steps):
+            i0, ng = step(args.warmup + kk, gev[kk])
+            timed_batches.extend(range(i0, i0 + ng))
+        end.record()
+        torch.cuda.synchronize()
+        if args.nvtx:
+            torch.cuda.nvtx.range_pop()
+    step_ms_local = start.elapsed_time(end)
+    gather_ms = sum(a.elapsed_time(b) for a, b in gev)
+    t = torch.tensor([step_ms_local], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    n_batches = len(timed_batches)
+    gpu_launches = args.steps * (1 + 1 + 2 + 3 * smp.L + 1)
+
+    # full-epoch accounting pass (remote rows/epoch, parity metric)
+    pipe.start_epoch(sched, 0)
+    eev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    eev[0].record()
+    for i0 in range(0, nb, G):
+        ng = min(G, nb - i0)
+        pipe.plan.fill(pipe.perm, 0, i0, ng)
+        smp.run(ng)
+        pipe.gather(ng, i0)
+    eev[1].record()
+    torch.cuda.synchronize()
+    epoch_ms = eev[0].elapsed_time(eev[1])
+    tot = pipe.totals()
+    per_batch = tot["per_batch"]
+    rows_b = per_batch[:, 0] + per_batch[:, 1] + per_batch[:, 2]
+    timed_rows = int(sum(rows_b[i] for i in timed_batches))
+
+    # roofline of the dominant kernel (bundle gather): read + write every row,
+    # plus the id and route word per row
+    peak, peak_src = peaks()
+    gather_bytes = timed_rows * (2 * 4 * d + 8)
+    achieved = gather_bytes / (gather_ms / 1e3) / 1e9
+    step_bytes = gather_bytes  # sampler bytes reported in DESIGN.md (~3% of the batch)
+
+    # e2e: host seeds in (pinned H2D), accounting out (D2H) per group
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(pipe, g, cfg, args, world)
+
+    result = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        hot_np = hot.cpu().numpy().astype(np.int64)
+        result = cpu_baseline(cpu_state(g, book, cfg, hot_np, part), args.cpu_seconds, nb)
+
+    agg_batches = n_batches * world
+    value = agg_batches / (total_ms / 1e3)
+    remote_rows = tot["hit"] + tot["fallback"]
+    if world > 1:
+        dist.barrier()
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+    line = {
+        "metric": METRIC, "value": value, "unit": "batches/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": (f"synthetic: gnnpipe.synth_powerlaw({cfg['n']}, {cfg['m']}, {cfg['d']}, "
+                 f"{cfg['classes']}, seed={S0}) reproduced bit-exactly + "
+                 f"partition_edgecut(k={k})"),
+        "config": {"workload": args.config, "batch_size": cfg["batch"], "fanouts": cfg["fanouts"],
+                   "partitions": k, "worker": part, "cache_pct": args.cache_pct, "n_hot": n_hot,
+                   "batches_per_step": G, "parallelism": f"worker-per-gpu x{world}",
+                   "l2": "inputs larger than L2 (feature shards %.0f MB; bundle %.0f MB/batch)"
+                         % (g.num_nodes * d * 4 / 1e6, float(rows_b.mean()) * d * 4 / 1e6)},
+        "roofline": {"kernel": "gather_bundle_kernel", "bound": "hbm", "achieved": achieved,
+                     "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": ncu_traffic("gather_bundle_kernel"),
+                     "bytes_per_launch": gather_bytes / args.steps,
+                     "share_of_step": gather_ms / step_ms_local,
+                     "step_frac": step_bytes / (step_ms_local / 1e3) / 1e9 / peak},
+        "e2e": e2e,
+        "gpu_launches": gpu_launches,
+        "clocks": clk.summary(),
+        "remote_rows_epoch": {"worker": part, "uncached": remote_rows,
+                              "fallback": tot["fallback"], "cache_hits": tot["hit"],
+                              "rpcs": tot["rpcs"], "reduction": remote_rows / max(1, tot["fallback"]),
+                              "bad": tot["bad"], "epoch_ms": epoch_ms, "plan_pass_ms": plan_ms},
+        "cpu_baseline": result,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(pipe, g, cfg, args, world):
+    """Public pipeline API with host buffers: each step copies the group's
+    seed ids + batch seeds from pinned host memory (H2D), samples and
+    gathers, and reads the per-batch accounting back (D2H, host-visible
+    before the next step).  The bundle rows stay in HBM for the on-device
+    consumer (model.py's aggregation), as in a GPU training loop."""
+    import torch
+    import torch.distributed as dist
+
+    from oracle import gnn_oracle as orc  # host batch seeds = BatchPlan.batch_seeds
+
+    G, nb, smp = pipe.G, pipe.nb, pipe.sampler
+    B = cfg["batch"]
+    perm = pipe.perm.cpu().numpy()
+    n_full = max(1, nb // G)
+    seeds_h = torch.zeros((n_full, G, smp.caps[0]), dtype=torch.int32).pin_memory()
+    nseeds_h = torch.zeros((n_full, G), dtype=torch.int32).pin_memory()
+    rng_h = torch.zeros((n_full, G), dtype=torch.int64).pin_memory()
+    for s in range(n_full):
+        for b in range(G):
+            i = s * G + b
+            chunk = perm[i * B:(i + 1) * B]
+            seeds_h[s, b, :len(chunk)] = torch.from_numpy(chunk.astype(np.int32))
+            nseeds_h[s, b] = len(chunk)
+            rng_h[s, b] = int(np.uint64(orc.batch_seed(S0, 0, i)).astype(np.int64))
+    out_h = torch.zeros((G, 8), dtype=torch.int32).pin_memory()
+
+    def one(kk):
+        s = kk % n_full
+        i0 = s * G
+        smp.seeds.copy_(seeds_h[s], non_blocking=True)
+        smp.nseeds.copy_(nseeds_h[s], non_blocking=True)
+        smp.rng.copy_(rng_h[s], non_blocking=True)
+        smp.run(G)
+        pipe.gather(G, i0)
+        out_h.copy_(pipe.counters[i0:i0 + G], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return int(out_h[:, 2].sum())
+
+    for kk in range(args.warmup):
+        one(kk)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t = time.perf_counter()
+    for kk in range(args.steps):
+        one(args.warmup + kk)
+    wall = time.perf_counter() - t
+    tt = torch.tensor([wall], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    wall = float(tt.item())
+    h2d = G * smp.caps[0] * 4 + G * 4 + G * 8
+    d2h = G * 8 * 4
+    return {"value": args.steps * G * world / wall, "unit": "batches/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "api": "WorkerPipeline: seeds from pinned host, accounting read back per step"}
+
+
+if __name__ == "__main__":
+    main()
