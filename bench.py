@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--nvtx", action="store_true", help="NVTX range 'timed' around the timed steps")
+    ap.add_argument("--serial", action="store_true",
+                    help="no sample/gather overlap (one stream, per-kernel timing)")
     return ap.parse_args()
 
 
@@ -270,7 +272,8 @@ def main():
         multigpu.exchange_shards(store, rank, world)
     store.build_route(shard_ids)
     train = np.flatnonzero(g.train_mask)
-    pipe = WorkerPipeline(dg, store, part, train, cfg["fanouts"], cfg["batch"], S0, args.group)
+    pipe = WorkerPipeline(dg, store, part, train, cfg["fanouts"], cfg["batch"], S0, args.group,
+                          nbuf=1 if args.serial else 2)
     nb, G = pipe.nb, pipe.G
     sched = SeedSchedule(S0, 1, nb)
 
@@ -295,6 +298,8 @@ def main():
 
     def step(kk, timed_events=None):
         i0 = (kk % n_full) * G
+        if not args.serial:
+            return i0, pipe.step_overlapped(i0)
         ng = min(G, nb - i0)
         pipe.plan.fill(pipe.perm, 0, i0, ng)
         smp.run(ng)
@@ -305,8 +310,10 @@ def main():
             timed_events[1].record()
         return i0, ng
 
+    pipe.enter_streams()
     for kk in range(args.warmup):
         step(kk)
+    pipe.sync_streams()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -320,15 +327,30 @@ def main():
         if args.nvtx:
             torch.cuda.nvtx.range_push("timed")
         start.record()
+        pipe.enter_streams()
         for kk in range(args.steps):
             i0, ng = step(args.warmup + kk, gev[kk])
             timed_batches.extend(range(i0, i0 + ng))
+        pipe.sync_streams()
         end.record()
         torch.cuda.synchronize()
         if args.nvtx:
             torch.cuda.nvtx.range_pop()
     step_ms_local = start.elapsed_time(end)
-    gather_ms = sum(a.elapsed_time(b) for a, b in gev)
+    if args.serial:
+        gather_ms = sum(a.elapsed_time(b) for a, b in gev)
+    else:
+        # overlapped run: time the gather alone on the same batches (serial)
+        for kk in range(args.steps):
+            i0 = ((args.warmup + kk) % n_full) * G
+            ng = min(G, nb - i0)
+            pipe.plan.fill(pipe.perm, 0, i0, ng)
+            smp.run(ng)
+            gev[kk][0].record()
+            pipe.gather(ng, i0)
+            gev[kk][1].record()
+        torch.cuda.synchronize()
+        gather_ms = sum(a.elapsed_time(b) for a, b in gev)
     t = torch.tensor([step_ms_local], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

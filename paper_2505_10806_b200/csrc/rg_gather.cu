@@ -11,6 +11,8 @@
 // 32 lanes busy (flattened row x vector index) and written back contiguously.
 // Source rows may live in this GPU's HBM or in a peer GPU's shard (NVLink
 // P2P pointer); the kernel does not distinguish.
+#include <cstdlib>
+
 #include "rg_common.cuh"
 
 namespace rg {
@@ -156,8 +158,13 @@ extern "C" int rg_gather_bundle(const int32_t* d_ids, const int32_t* d_nids, int
   const int dq = 32 / nvec, dr = 32 % nvec;
   // enough CTAs for ~4 resident per SM on the largest slot; extra CTAs of a
   // short batch exit after one bounds check.
+  static const int ctas_per_sm = [] {
+    const char* e = getenv("RG_GATHER_CTAS_PER_SM");
+    return e ? std::max(1, atoi(e)) : 8;
+  }();
   const int64_t want = (cap + kGatherWarps * 32 - 1) / (kGatherWarps * 32);
-  const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(want, (kNumSMs * 8 + G - 1) / G));
+  const int gx = (int)std::max<int64_t>(
+      1, std::min<int64_t>(want, ((int64_t)kNumSMs * ctas_per_sm + G - 1) / G));
   gather_bundle_kernel<<<dim3(gx, G), kGatherWarps * 32, 0, (cudaStream_t)stream>>>(
       d_ids, d_nids, cap, d_route, bases, stride, nvec, dq, dr, my_part, d_out, d_counters);
   return check_launch("gather_bundle");

@@ -72,15 +72,122 @@ __device__ __forceinline__ int select_positions(uint64_t nk, int D, int T) {
   return pos;
 }
 
+// D <= 32 < ... : the take smallest of (at most) 32 distinct keys, one per
+// lane, by an MSB-first radix select on ballots; returns the lane mask.
+// Distinct keys make it terminate after ~log2(32) informative bits.
+__device__ __forceinline__ unsigned select_mask32(uint64_t key, unsigned cand, int need) {
+  unsigned sel = 0;
+  const uint32_t hi = (uint32_t)(key >> 32), lo = (uint32_t)key;
+#pragma unroll 1
+  for (int bit = 63; bit >= 0; --bit) {
+    const uint32_t w = bit >= 32 ? hi : lo;
+    const unsigned ones = __ballot_sync(kFull, (w >> (bit & 31)) & 1u);
+    const unsigned zeros = cand & ~ones;
+    const int nz = __popc(zeros);
+    if (nz >= need) {
+      cand = zeros;
+    } else {
+      sel |= zeros;
+      need -= nz;
+      cand &= ones;
+    }
+    if (__popc(cand) == need) return sel | cand;
+  }
+  return sel;
+}
+
+// Same over up to 64 keys, two per lane (k0: candidate lane, k1: 32+lane).
+__device__ __forceinline__ void select_mask64(uint64_t k0, uint64_t k1, unsigned c0, unsigned c1,
+                                              int need, unsigned& s0, unsigned& s1) {
+  s0 = 0;
+  s1 = 0;
+#pragma unroll 1
+  for (int bit = 63; bit >= 0; --bit) {
+    const unsigned o0 = __ballot_sync(kFull, (k0 >> bit) & 1ull);
+    const unsigned o1 = __ballot_sync(kFull, (k1 >> bit) & 1ull);
+    const unsigned z0 = c0 & ~o0, z1 = c1 & ~o1;
+    const int nz = __popc(z0) + __popc(z1);
+    if (nz >= need) {
+      c0 = z0;
+      c1 = z1;
+    } else {
+      s0 |= z0;
+      s1 |= z1;
+      need -= nz;
+      c0 &= o0;
+      c1 &= o1;
+    }
+    if (__popc(c0) + __popc(c1) == need) {
+      s0 |= c0;
+      s1 |= c1;
+      return;
+    }
+  }
+}
+
+// D > 32 >= T: a threshold t0 with E[#keys < t0] = T + 3 sqrt(T) + 3 (keys
+// are uniform 64-bit values) keeps ~T..T+20 candidates; they are streamed
+// into shared memory in position order and the T smallest are radix-
+// selected among them.  Exact whenever T <= #candidates <= 64 (every
+// non-candidate key is >= t0 > every candidate key); otherwise (rare)
+// returns false and the caller uses the running top-T list.
+// On success lanes hold the selected positions compacted in position
+// order: *nsel = T, selected position r is returned by lane r (r < T).
+__device__ __forceinline__ bool select_threshold(uint64_t nk, int D, int T, uint64_t* s_key,
+                                                 int32_t* s_pos, int& pos_out) {
+  const int lane = lane_id();
+  const unsigned lt = (1u << lane) - 1u;
+  const double mu = (double)T + 3.0 * sqrt((double)T) + 3.0;
+  const double frac = mu / (double)D;
+  const uint64_t t0 = frac >= 1.0 ? ~0ull : (uint64_t)(frac * 18446744073709551616.0);
+  int count = 0;
+  uint64_t kk = nk + (uint64_t)(lane + 1) * GOLDEN;
+  const uint64_t step = 32ull * GOLDEN;
+  for (int base = 0; base < D; base += 32) {
+    const uint64_t key = mix64(kk);
+    kk += step;
+    const bool c = base + lane < D && key < t0;
+    const unsigned m = __ballot_sync(kFull, c);
+    if (c) {
+      const int off = count + __popc(m & lt);
+      if (off < 64) {
+        s_key[off] = key;
+        s_pos[off] = base + lane;
+      }
+    }
+    count += __popc(m);
+  }
+  __syncwarp();
+  if (count < T || count > 64) return false;
+  const uint64_t k0 = lane < count ? s_key[lane] : ~0ull;
+  const uint64_t k1 = 32 + lane < count ? s_key[32 + lane] : ~0ull;
+  const unsigned c0 = __ballot_sync(kFull, lane < count);
+  const unsigned c1 = __ballot_sync(kFull, 32 + lane < count);
+  unsigned s0, s1;
+  select_mask64(k0, k1, c0, c1, T, s0, s1);
+  // compact the selected candidates (already in position order) to lanes
+  const int n0 = __popc(s0);
+  if ((s0 >> lane) & 1u) s_pos[64 + __popc(s0 & lt)] = s_pos[lane];
+  if ((s1 >> lane) & 1u) s_pos[64 + n0 + __popc(s1 & lt)] = s_pos[32 + lane];
+  __syncwarp();
+  pos_out = lane < T ? s_pos[64 + lane] : 0;
+  __syncwarp();
+  return true;
+}
+
 __global__ void __launch_bounds__(kSampleWarps * 32)
     sample_level_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                         int G, const int32_t* __restrict__ front, int64_t cap_in,
                         const int32_t* __restrict__ nfront, int F, uint64_t level_mix,
                         const uint64_t* __restrict__ rng_seed, int32_t* __restrict__ ell,
                         int32_t* __restrict__ cnt, uint32_t* __restrict__ bm, int64_t nwords,
-                        int32_t* __restrict__ slow) {
+                        int32_t* __restrict__ slow, int sorted_rows) {
   __shared__ int s_next;
+  __shared__ uint64_t s_key[kSampleWarps][64];
+  __shared__ int32_t s_pos[kSampleWarps][96];
   const int lane = lane_id();
+  const int warp = threadIdx.x >> 5;
+  const unsigned lt_mask = (1u << lane) - 1u;
   int maxf = 0;
   for (int b = lane; b < G; b += 32) maxf = max(maxf, nfront[b]);
 #pragma unroll
@@ -113,19 +220,58 @@ __global__ void __launch_bounds__(kSampleWarps * 32)
       }
       continue;
     }
-    int32_t nb = INT_MAX;
-    if (D <= F) {
-      if (lane < D) nb = __ldg(indices + a + lane);
-    } else {
-      const uint64_t sd = mix64(rng_seed[b] ^ level_mix);
-      const uint64_t nk = mix64(((uint64_t)v + 1ull) * GOLDEN ^ sd);
-      const int pos = select_positions(nk, D, T);
-      if (lane < T) nb = __ldg(indices + a + pos);
+    int32_t* out = ell + row * F;
+    uint32_t* bmb = bm + (int64_t)b * nwords;
+    if (D <= 32) {
+      // one chunk: lane p owns position p
+      unsigned sel;
+      if (D <= F) {
+        sel = D == 32 ? kFull : ((1u << D) - 1u);
+      } else {
+        const uint64_t sd = mix64(rng_seed[b] ^ level_mix);
+        const uint64_t nk = mix64(((uint64_t)v + 1ull) * GOLDEN ^ sd);
+        const uint64_t key = lane < D ? mix64(nk + (uint64_t)(lane + 1) * GOLDEN) : ~0ull;
+        sel = select_mask32(key, __ballot_sync(kFull, lane < D), T);
+      }
+      const bool mine = (sel >> lane) & 1u;
+      int32_t nb = mine ? __ldg(indices + a + lane) : INT_MAX;
+      if (sorted_rows) {
+        // ascending CSR row: position order is id order
+        if (mine) {
+          out[__popc(sel & lt_mask)] = nb;
+          mark(bmb, nb);
+        }
+        continue;
+      }
+      warp_bitonic_sort_keys(nb);
+      if (lane < T) {
+        out[lane] = nb;
+        mark(bmb, nb);
+      }
+      continue;
     }
+    // D > 32 (> F): threshold candidates, else the running top-T list
+    const uint64_t sd = mix64(rng_seed[b] ^ level_mix);
+    const uint64_t nk = mix64(((uint64_t)v + 1ull) * GOLDEN ^ sd);
+    int pos;
+    const bool ordered = select_threshold(nk, D, T, s_key[warp], s_pos[warp], pos);
+    if (!ordered) pos = select_positions(nk, D, T);
+    int32_t nb = INT_MAX;
+    if (sorted_rows) {
+      int p = lane < T ? pos : INT_MAX;
+      if (!ordered) warp_bitonic_sort_keys(p);
+      if (lane < T) {
+        nb = __ldg(indices + a + p);
+        out[lane] = nb;
+        mark(bmb, nb);
+      }
+      continue;
+    }
+    if (lane < T) nb = __ldg(indices + a + pos);
     warp_bitonic_sort_keys(nb);
     if (lane < T) {
-      ell[row * F + lane] = nb;
-      mark(bm + (int64_t)b * nwords, nb);
+      out[lane] = nb;
+      mark(bmb, nb);
     }
   }
 }
@@ -248,15 +394,21 @@ __global__ void __launch_bounds__(kCompactThreads)
   if (threadIdx.x == 0) chunk_tot[(int64_t)b * nchunks + blockIdx.x] = tot;
 }
 
+// Emission is warp-cooperative: each warp owns kCompactWords/8 consecutive
+// words; for every word the 32 lanes test one bit each and the set bits are
+// written with one coalesced store (ballot + prefix popcount).
 __global__ void __launch_bounds__(kCompactThreads)
     bitmap_emit_kernel(const uint32_t* __restrict__ bm, int64_t nwords, int64_t nchunks,
                        const int32_t* __restrict__ chunk_tot, int32_t* __restrict__ out,
                        int64_t cap_out, int32_t* __restrict__ nout, int32_t* __restrict__ wpre) {
+  constexpr int kWarps = kCompactThreads / 32;
+  constexpr int kPerWarp = kCompactWords / kWarps;  // 128 words
   __shared__ int s_red[32];
   __shared__ int s_base;
+  __shared__ int s_warp[kWarps];
   const int b = blockIdx.y;
   const int64_t chunk = blockIdx.x;
-  // base = sum of the preceding chunk totals (and the grand total for CTA 0)
+  const int lane = lane_id(), warp = threadIdx.x >> 5;
   int before = 0, all = 0;
   for (int64_t c = threadIdx.x; c < nchunks; c += blockDim.x) {
     const int t = chunk_tot[(int64_t)b * nchunks + c];
@@ -267,37 +419,55 @@ __global__ void __launch_bounds__(kCompactThreads)
   block_excl_scan<kCompactThreads>(before, s_red, &tot);
   if (threadIdx.x == 0) s_base = tot;
   __syncthreads();
-  const int base = s_base;
-  __syncthreads();
   if (chunk == 0) {
     int grand;
     block_excl_scan<kCompactThreads>(all, s_red, &grand);
     if (threadIdx.x == 0) nout[b] = grand;
   }
   const uint32_t* w = bm + (int64_t)b * nwords;
-  const int64_t w0 = chunk * kCompactWords + threadIdx.x * 4;
-  uint32_t words[4];
-  int c = 0;
+  const int64_t wbase = chunk * kCompactWords + (int64_t)warp * kPerWarp;
+  uint32_t words[kPerWarp / 32];
+  int wsum = 0;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    words[i] = (w0 + i < nwords) ? w[w0 + i] : 0u;
-    c += __popc(words[i]);
+  for (int g = 0; g < kPerWarp / 32; ++g) {
+    const int64_t wi = wbase + g * 32 + lane;
+    words[g] = wi < nwords ? w[wi] : 0u;
+    wsum += __popc(words[g]);
   }
-  int dummy;
-  int at = base + block_excl_scan<kCompactThreads>(c, s_red, &dummy);
-  int32_t* o = out + (int64_t)b * cap_out;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    if (w0 + i >= nwords) break;
-    if (wpre) wpre[(int64_t)b * nwords + w0 + i] = at;
-    uint32_t m = words[i];
-    const int32_t id0 = (int32_t)((w0 + i) * 32);
-    while (m) {
-      const int bit = __ffs(m) - 1;
-      m &= m - 1;
-      if (at < cap_out) o[at] = id0 + bit;
-      ++at;
+  for (int o = 16; o; o >>= 1) wsum += __shfl_xor_sync(kFull, wsum, o);
+  if (lane == 0) s_warp[warp] = wsum;
+  __syncthreads();
+  int at = s_base;
+  for (int i = 0; i < warp; ++i) at += s_warp[i];
+  int32_t* o = out + (int64_t)b * cap_out;
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int g = 0; g < kPerWarp / 32; ++g) {
+    // exclusive prefix of this group's word popcounts
+    const int c = __popc(words[g]);
+    int x = c;
+#pragma unroll
+    for (int s2 = 1; s2 < 32; s2 <<= 1) {
+      const int y = __shfl_up_sync(kFull, x, s2);
+      if (lane >= s2) x += y;
     }
+    const int pre = at + x - c;
+    const int64_t wi = wbase + g * 32 + lane;
+    if (wpre && wi < nwords) wpre[(int64_t)b * nwords + wi] = pre;
+    const int gsum = __shfl_sync(kFull, x, 31);
+    unsigned any = __ballot_sync(kFull, c != 0);
+    while (any) {
+      const int jw = __ffs(any) - 1;
+      any &= any - 1;
+      const uint32_t word = __shfl_sync(kFull, words[g], jw);
+      const int off = __shfl_sync(kFull, pre, jw);
+      if ((word >> lane) & 1u) {
+        const int pos = off + __popc(word & lt);
+        if (pos < cap_out) o[pos] = (int32_t)((wbase + g * 32 + jw) * 32 + lane);
+      }
+    }
+    at += gsum;
   }
 }
 
@@ -402,7 +572,8 @@ extern "C" int rg_sample_level(const int64_t* d_indptr, const int32_t* d_indices
                                int32_t G, const int32_t* d_front, int64_t cap_in,
                                const int32_t* d_nfront, int32_t fanout, int32_t level,
                                const uint64_t* d_rng_seed, int32_t* d_ell, int32_t* d_cnt,
-                               uint32_t* d_bm, int64_t nwords, int32_t* d_slow, void* stream) {
+                               uint32_t* d_bm, int64_t nwords, int32_t* d_slow,
+                               int32_t sorted_rows, void* stream) {
   RG_REQUIRE(G >= 1 && cap_in >= 1 && n >= 1, "rg_sample_level: bad sizes");
   RG_REQUIRE(fanout >= 1, "rg_sample_level: fanout must be >= 1");
   if (fanout > kSlowCap) {
@@ -415,10 +586,11 @@ extern "C" int rg_sample_level(const int64_t* d_indptr, const int32_t* d_indices
   int32_t* slow = fanout > 32 ? d_slow : nullptr;
   if (slow && cudaMemsetAsync(slow, 0, sizeof(int32_t), s) != cudaSuccess)
     return check_launch("sample_level memset");
-  const int grid = kNumSMs * 4;
+  const int grid = kNumSMs * 5;  // 48 regs x 256 threads: 5 CTAs per SM
   sample_level_kernel<<<grid, kSampleWarps * 32, 0, s>>>(d_indptr, d_indices, G, d_front, cap_in,
                                                          d_nfront, fanout, level_mix, d_rng_seed,
-                                                         d_ell, d_cnt, d_bm, nwords, slow);
+                                                         d_ell, d_cnt, d_bm, nwords, slow,
+                                                         sorted_rows);
   int rc = check_launch("sample_level");
   if (rc || !slow) return rc;
   sample_slow_kernel<<<kNumSMs, 256, 0, s>>>(d_indptr, d_indices, G, d_front, cap_in, fanout,

@@ -34,6 +34,19 @@ def _cur() -> int:
     return _lib.stream_handle()
 
 
+def rows_sorted(indptr: np.ndarray, indices: np.ndarray) -> bool:
+    """True if every CSR row is nondecreasing (lets the sampler skip its sort)."""
+    indices = np.asarray(indices)
+    if len(indices) < 2:
+        return True
+    desc = np.flatnonzero(np.diff(indices.astype(np.int64)) < 0) + 1
+    if len(desc) == 0:
+        return True
+    # a decrease is allowed only where a new row starts
+    starts = np.asarray(indptr, dtype=np.int64)
+    return bool(np.isin(desc, starts).all())
+
+
 class DeviceGraph:
     """CSR graph in HBM: indptr int64, indices int32 (ids < 2^31)."""
 
@@ -47,6 +60,7 @@ class DeviceGraph:
         self.indptr = torch.from_numpy(np.ascontiguousarray(indptr, dtype=np.int64)).to(self.device)
         self.indices = torch.from_numpy(np.ascontiguousarray(indices, dtype=np.int32)).to(self.device)
         self.num_edges = int(self.indices.numel())
+        self.sorted_rows = rows_sorted(indptr, indices)
 
     @classmethod
     def of(cls, g) -> "DeviceGraph":
@@ -119,7 +133,7 @@ class BlockSampler:
             _lib.call("rg_sample_level", ptr(dg.indptr), ptr(dg.indices), dg.n, G,
                       ptr(self.front[d]), self.caps[d], ptr(self.nfront[d]), self.step_fan[d], d,
                       ptr(self.rng), ptr(self.ell[d]), ptr(self.cnt[d]), ptr(self.bm), dg.nwords,
-                      ptr(self.slow), s)
+                      ptr(self.slow), int(dg.sorted_rows), s)
             _lib.call("rg_bitmap_compact", ptr(self.bm), dg.nwords, G, ptr(self.chunk),
                       ptr(self.front[d + 1]), self.caps[d + 1], ptr(self.nfront[d + 1]), None, s)
 

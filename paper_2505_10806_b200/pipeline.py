@@ -46,8 +46,13 @@ def resolve_n_hot(pct: float, num_remote: int) -> int:
 
 
 class WorkerPipeline:
+    """nbuf = 2 double-buffers the sampler state and the bundle slots so
+    that sampling of group k+1 (latency/ALU-bound) runs on one stream while
+    the gather of group k (HBM-bound) runs on another — the device form of
+    the reference's one-batch-ahead prefetch (prefetch.py:91-164)."""
+
     def __init__(self, dg: DeviceGraph, store: FeatureStore, my_part: int, train_nodes: np.ndarray,
-                 fanouts, batch_size: int, s0: int, group: int):
+                 fanouts, batch_size: int, s0: int, group: int, nbuf: int = 2):
         self.dg, self.store, self.my_part = dg, store, int(my_part)
         self.plan = PlanPass(dg, train_nodes, fanouts, batch_size, s0, group=group)
         self.sampler: BlockSampler = self.plan.sampler
@@ -55,8 +60,17 @@ class WorkerPipeline:
         self.nb = self.plan.nb
         smp = self.sampler
         self.cap_in = smp.caps[smp.L]
-        self.rows = torch.empty((self.G, self.cap_in, store.stride), dtype=torch.float32,
-                                device=dg.device)
+        self.nbuf = int(nbuf)
+        self.samplers = [smp] + [BlockSampler(dg, fanouts, batch_size, group=self.G)
+                                 for _ in range(self.nbuf - 1)]
+        self.row_bufs = [torch.empty((self.G, self.cap_in, store.stride), dtype=torch.float32,
+                                     device=dg.device) for _ in range(self.nbuf)]
+        self.rows = self.row_bufs[0]
+        self.s_sample = torch.cuda.Stream()
+        self.s_gather = torch.cuda.Stream()
+        self.ev_sampled = [torch.cuda.Event() for _ in range(self.nbuf)]
+        self.ev_gathered = [torch.cuda.Event() for _ in range(self.nbuf)]
+        self.k = 0
         # per-batch provenance counters of the current epoch (nb x 8)
         self.counters = torch.zeros((self.nb, _lib.RG_NCOUNTERS), dtype=I32, device=dg.device)
         self.cache: HotCache | None = None
@@ -108,8 +122,41 @@ class WorkerPipeline:
         self.launches += 1 + 1 + 2 + smp.L * 3 + 1
         return ng
 
-    def gather(self, ng: int, i0: int) -> None:
-        smp, st = self.sampler, self.store
+    def step_overlapped(self, i0: int) -> int:
+        """Like step(), but sampling and gather of consecutive groups overlap
+        on two streams (buffer k % nbuf).  Call sync_streams() before reading
+        results on the current stream."""
+        ng = min(self.G, self.nb - i0)
+        slot = self.k % self.nbuf
+        self.k += 1
+        smp = self.samplers[slot]
+        with torch.cuda.stream(self.s_sample):
+            self.s_sample.wait_event(self.ev_gathered[slot])  # slot free again
+            self.plan.fill(self.perm, self.epoch, i0, ng, smp)
+            smp.run(ng)
+            self.ev_sampled[slot].record(self.s_sample)
+        with torch.cuda.stream(self.s_gather):
+            self.s_gather.wait_event(self.ev_sampled[slot])
+            self.gather(ng, i0, smp, self.row_bufs[slot])
+            self.ev_gathered[slot].record(self.s_gather)
+        self.launches += 1 + 1 + 2 + smp.L * 3 + 1
+        return ng
+
+    def enter_streams(self) -> None:
+        """Order both side streams after the current stream's work."""
+        cur = torch.cuda.current_stream()
+        self.s_sample.wait_stream(cur)
+        self.s_gather.wait_stream(cur)
+
+    def sync_streams(self) -> None:
+        cur = torch.cuda.current_stream()
+        cur.wait_stream(self.s_sample)
+        cur.wait_stream(self.s_gather)
+
+    def gather(self, ng: int, i0: int, smp=None, rows=None) -> None:
+        smp = smp or self.sampler
+        rows = self.rows if rows is None else rows
+        st = self.store
         bases = list(st.bases)
         route = st.route
         if self.cache is not None and self.cache.hot_ids.numel():
@@ -117,7 +164,7 @@ class WorkerPipeline:
             route = self.cache.route
         _lib.call("rg_gather_bundle", ptr(smp.front[smp.L]), ptr(smp.nfront[smp.L]), self.cap_in,
                   ng, ptr(route), bases_array(bases).ctypes.data, st.stride, self.my_part,
-                  ptr(self.rows), ptr(self.counters) + i0 * _lib.RG_NCOUNTERS * 4,
+                  ptr(rows), ptr(self.counters) + i0 * _lib.RG_NCOUNTERS * 4,
                   _lib.stream_handle())
 
     def totals(self) -> dict:
@@ -129,3 +176,85 @@ class WorkerPipeline:
         return {"local": int(c[:, 0].sum()), "hit": int(c[:, 1].sum()),
                 "fallback": int(c[:, 2].sum()), "bad": int(c[:, 4].sum()), "rpcs": rpcs,
                 "per_batch": c}
+
+
+def run_accounting(g, book, fanouts, batch_size: int, epochs: int, s0: int, mode: str = "rapid",
+                   n_hot: int | None = None, n_hot_pct: float = 15.0, hot_scope: str = "epoch",
+                   workers=None, group: int = 16, features: bool = True) -> dict:
+    """Per-worker, per-epoch data-path accounting of the reference's worker
+    loop (train.py:171-264 without the SGD step): rpc_calls, nodes_pulled,
+    bytes_pulled, cache_hits, cache_misses, reuse_ratio, plus the cache
+    fill account.  Every batch really is sampled and gathered on the
+    device; only the training consumer is absent.
+
+    Semantics reproduced: n_hot = int(#remote(all epochs) * pct / 100)
+    (train.py:165-168); epoch scope installs top_hot(collect_access(e)) for
+    each epoch via the double buffer, resetting hit/miss counters on each
+    successful swap; global scope builds one set and never swaps, so its
+    counters accumulate (cache.py:116-129); baseline mode has no cache,
+    misses = nodes pulled and reuse 0.0 or None (train.py:238-240)."""
+    if mode not in ("baseline", "rapid") or hot_scope not in ("epoch", "global"):
+        raise ValueError("bad mode / hot scope")
+    owner = np.asarray(book.owner)
+    k = int(book.k)
+    dg = DeviceGraph.of(g)
+    d = int(g.feat_dim) if features else 4
+    store = FeatureStore(owner, k, d)
+    shard_ids = [np.flatnonzero(owner == q) for q in range(k)]
+    for q in range(k):
+        rows = (g.features[shard_ids[q]] if features
+                else np.zeros((len(shard_ids[q]), d), dtype=np.float32))
+        store.set_shard(q, FeatureStore.pad_rows(rows, store.stride, dg.device))
+    store.build_route(shard_ids)
+    train = np.flatnonzero(g.train_mask)
+    workers = list(range(k)) if workers is None else list(workers)
+    pipe0 = WorkerPipeline(dg, store, workers[0], train, fanouts, batch_size, s0, group, nbuf=1)
+    nb = pipe0.nb
+    sched = SeedSchedule(s0, epochs, nb)
+    counts = [pipe0.count_epoch(sched, e) for e in range(epochs)]
+    counts_all = counts[0].clone()
+    for c in counts[1:]:
+        counts_all += c
+    max_count = max(1, nb * epochs)
+    out = {}
+    for p in workers:
+        pipe = pipe0 if p == workers[0] else WorkerPipeline(dg, store, p, train, fanouts,
+                                                            batch_size, s0, group, nbuf=1)
+        pipe.my_part = p
+        fill = [0, 0, 0]
+        nh = 0
+        if mode == "rapid":
+            _, nout, _, _ = candidates(counts_all, store.owner, p, max_count)
+            nh = n_hot if n_hot is not None else resolve_n_hot(n_hot_pct, int(nout.item()))
+        hits_acc = misses_acc = 0
+        recs = []
+        for e in range(epochs):
+            if mode == "rapid" and (hot_scope == "epoch" or e == 0):
+                scope_counts = counts[e] if hot_scope == "epoch" else counts_all
+                hot = pipe.select_hot(scope_counts, nh, max_count)
+                cache = pipe.build_cache(hot)
+                if cache.fill[1]:  # an empty pull is free (store.py:181-182)
+                    fill = [fill[0] + cache.fill[0], fill[1] + cache.fill[1],
+                            fill[2] + 4 * int(g.feat_dim) * cache.fill[1]]
+            pipe.start_epoch(sched, e)
+            for i0 in range(0, nb, pipe.G):
+                pipe.step(i0)
+            t = pipe.totals()
+            nodes = t["fallback"]
+            if mode == "rapid":
+                if hot_scope == "epoch":
+                    hits, misses = t["hit"], t["fallback"]
+                else:
+                    hits_acc += t["hit"]
+                    misses_acc += t["fallback"]
+                    hits, misses = hits_acc, misses_acc
+                reuse = hits / (hits + misses) if hits + misses else None
+            else:
+                hits, misses = 0, nodes
+                reuse = 0.0 if misses else None
+            recs.append({"rpc_calls": t["rpcs"], "nodes_pulled": nodes,
+                         "bytes_pulled": 4 * int(g.feat_dim) * nodes, "cache_hits": hits,
+                         "cache_misses": misses, "reuse_ratio": reuse, "n_hot": nh,
+                         "local": t["local"]})
+        out[p] = {"records": recs, "fill": fill}
+    return out

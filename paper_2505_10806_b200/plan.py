@@ -101,8 +101,8 @@ class PlanPass:
     def permutation(self, schedule: SeedSchedule, e: int) -> torch.Tensor:
         return epoch_order_device(self.train, epoch_master(schedule, e))
 
-    def fill(self, perm: torch.Tensor, e: int, i0: int, G: int) -> None:
-        smp = self.sampler
+    def fill(self, perm: torch.Tensor, e: int, i0: int, G: int, smp=None) -> None:
+        smp = smp or self.sampler
         _lib.call("rg_fill_seeds", ptr(perm), self.n_train, self.batch_size, i0, G, ptr(smp.seeds),
                   ptr(smp.nseeds), smp.caps[0], self.s0 & (2**64 - 1), e, ptr(smp.rng),
                   _lib.stream_handle())

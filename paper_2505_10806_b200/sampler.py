@@ -8,6 +8,7 @@ expansion).  Results are bit-identical to the reference.
 
 from __future__ import annotations
 
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -91,14 +92,17 @@ class ComputationBlock:
 
 
 def _sampler_for(dg: DeviceGraph, fanouts, n_seeds: int) -> BlockSampler:
+    """Per-thread cached sampler (its device buffers are per-call scratch,
+    so concurrent callers — e.g. the Prefetcher's producer thread and the
+    consumer — must not share one)."""
     cap = 1
     while cap < n_seeds:
         cap <<= 1
-    key = (tuple(int(f) for f in fanouts), cap)
+    key = (tuple(int(f) for f in fanouts), cap, threading.get_ident())
     cache = dg.__dict__.setdefault("_samplers", {})
     smp = cache.get(key)
     if smp is None:
-        if len(cache) > 8:
+        if len(cache) > 16:
             cache.clear()
         smp = BlockSampler(dg, fanouts, cap, group=1)
         cache[key] = smp

@@ -1,0 +1,396 @@
+"""Device parity: the CUDA path (through the C ABI) against the reference's
+golden outputs and the CPU oracle.  Bit-exact for every id, count, set and
+row; the reference's own REPLAY log is reproduced end to end."""
+
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import fixture_graph, load_case
+from oracle import gnn_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def rg():
+    import paper_2505_10806_b200 as rg
+
+    from paper_2505_10806_b200 import _lib
+
+    _lib.device()  # loud failure if the extension or the GPU is missing
+    return rg
+
+
+@pytest.fixture(scope="module")
+def small(rg):
+    return rg.synth_powerlaw(1000, 5, 8, 4, seed=7)
+
+
+def test_native_library_is_loaded(rg):
+    from paper_2505_10806_b200 import _lib
+
+    lib = _lib.device()
+    assert lib.rg_device_ok() == 1
+    assert str(_lib.LIB_PATH).endswith("librapidgnn_b200.so")
+
+
+def test_mix64_and_stream_keys(rg):
+    from paper_2505_10806_b200 import _lib
+
+    x = np.array([0, 1, 2, 2**63, 2**64 - 1, 12345678901234567], dtype=np.uint64)
+    t = torch.from_numpy(x.view(np.int64)).cuda()
+    out = torch.empty_like(t)
+    _lib.call("rg_mix64", t.data_ptr(), out.data_ptr(), len(x), _lib.stream_handle())
+    assert np.array_equal(out.cpu().numpy().view(np.uint64), orc.mix_v(x))
+    keys = torch.empty(1000, dtype=torch.int64, device="cuda")
+    _lib.call("rg_stream_keys", 0xDEADBEEF12345678, 1000, keys.data_ptr(), _lib.stream_handle())
+    assert np.array_equal(keys.cpu().numpy().view(np.uint64),
+                          orc.counter_stream(0xDEADBEEF12345678, 1000))
+
+
+def test_sample_cases_bit_exact(rg, golden, small_npz, small):
+    for c in golden["sample_cases"]:
+        meta, seeds, fr, ed = load_case(small_npz, golden, c["name"])
+        g = small if meta["graph"] == "small" else fixture_graph(meta["graph"])
+        b = rg.sample_block(g, seeds, meta["fanouts"], int(meta["seed"]))
+        assert len(b.frontiers) == len(fr)
+        for a, w in zip(b.frontiers, fr):
+            assert np.array_equal(a, w), c["name"]
+        for (s1, d1), (s2, d2) in zip(b.edges, ed):
+            assert np.array_equal(s1, s2) and np.array_equal(d1, d2), c["name"]
+        assert np.array_equal(b.seeds, seeds)
+
+
+def test_unsorted_rows_path(rg):
+    """CSR rows that are not ascending take the sorting path; same result."""
+    rng = np.random.default_rng(5)
+    g = rg.synth_powerlaw(3000, 6, 4, 2, seed=3)
+    perm_idx = g.indices.copy()
+    for v in range(g.num_nodes):
+        a, b = g.indptr[v], g.indptr[v + 1]
+        perm_idx[a:b] = rng.permutation(perm_idx[a:b])
+    g2 = rg.Graph(g.num_nodes, g.num_edges, g.indptr, perm_idx, g.features, g.labels, g.feat_dim,
+                  g.num_classes, g.train_mask, g.val_mask, g.test_mask)
+    for s in range(4):
+        seeds = rng.choice(3000, 128, replace=False)
+        b = rg.sample_block(g2, seeds, [7, 40], s)
+        fr, ed = orc.block(g2.indptr, g2.indices, seeds, [7, 40], s)
+        for a, w in zip(b.frontiers, fr):
+            assert np.array_equal(a, w)
+        for (s1, d1), (s2, d2) in zip(b.edges, ed):
+            assert np.array_equal(s1, s2) and np.array_equal(d1, d2)
+
+
+def test_sampler_errors(rg, small):
+    with pytest.raises(ValueError):
+        rg.sample_block(small, np.array([], dtype=np.int64), [3], 0)
+    with pytest.raises(ValueError):
+        rg.sample_block(small, np.array([0]), [], 0)
+    with pytest.raises(ValueError):
+        rg.sample_block(small, np.array([small.num_nodes]), [3], 0)
+    with pytest.raises(NotImplementedError):
+        rg.sample_block(small, np.array([0]), [5000], 0)
+
+
+def test_epoch_batches(rg, golden, small_npz, small):
+    train = np.flatnonzero(small.train_mask)
+    sch = rg.SeedSchedule(s0=7, epochs=3, batches_per_epoch=-(-len(train) // 64))
+    for e in range(3):
+        assert np.array_equal(np.concatenate(rg.epoch_batches(train, 64, sch, e)),
+                              small_npz[f"perm_e{e}"])
+    big = rg.epoch_batches(np.arange(153_431), 1000, rg.SeedSchedule(1, 1, 154), 0)
+    flat = np.concatenate(big)
+    assert len(big) == 154 and len(big[-1]) == 431
+    want = golden["epoch_153431"]["hash"]
+    assert hashlib.blake2b(flat.astype("<i8").tobytes(), digest_size=16).hexdigest() == want
+    with pytest.raises(ValueError):
+        rg.epoch_batches(np.empty(0, dtype=np.int64), 10, sch, 0)
+    with pytest.raises(ValueError):
+        rg.epoch_batches(np.arange(5), 0, sch, 0)
+
+
+@pytest.fixture(scope="module")
+def plan_small(rg, small):
+    train = np.flatnonzero(small.train_mask)
+    return rg.generate_plan(small, train, [3, 5], 64, 3, s0=7)
+
+
+def test_generate_plan_matches_reference(plan_small, golden, small_npz):
+    assert plan_small.digest_hex() == golden["plan_small"]["digest"]
+    for e in range(3):
+        off, flat = small_npz[f"plan_off_e{e}"], small_npz[f"plan_in_e{e}"]
+        for i, s in enumerate(plan_small.input_sets[e]):
+            assert np.array_equal(s, flat[off[i]:off[i + 1]])
+    blk = plan_small.block(1, 3)
+    assert np.array_equal(blk.input_nodes, plan_small.input_sets[1][3])
+    assert blk.epoch == 1 and blk.batch == 3
+
+
+def test_collect_access_and_top_hot(rg, plan_small, small_npz):
+    book = rg.PartitionBook(k=2, owner=small_npz["owner2"])
+    for p in range(2):
+        for scope in (None, 0, 1, 2):
+            f = rg.collect_access(plan_small, book, p, epoch=scope)
+            tag = f"p{p}_{'all' if scope is None else 'e%d' % scope}"
+            assert np.array_equal(f.ids, small_npz[f"freq_ids_{tag}"])
+            assert np.array_equal(f.counts, small_npz[f"freq_cnt_{tag}"])
+            for n_hot in (0, 1, 5, 20, 80, len(f) - 1, len(f), len(f) + 5):
+                key = f"hot_{tag}_{n_hot}"
+                if key in small_npz.files:
+                    assert np.array_equal(rg.top_hot(f, n_hot), small_npz[key]), key
+
+
+def test_top_hot_kats_device(rg):
+    F = rg.FrequencyTable
+    assert rg.top_hot(F(np.array([2, 5, 9, 11]), np.array([4, 1, 7, 4])), 2).tolist() == [2, 9]
+    assert rg.top_hot(F(np.array([3, 8, 12]), np.array([5, 5, 5])), 2).tolist() == [3, 8]
+    assert rg.top_hot(F(np.array([1, 2]), np.array([1, 2])), 10).tolist() == [1, 2]
+    assert rg.top_hot(F(np.array([1, 2]), np.array([1, 2])), 0).tolist() == []
+    with pytest.raises(ValueError):
+        rg.top_hot(F(np.array([1]), np.array([1])), -1)
+    # brute force optimum with least-id ties (test_acceptance.py:347-359)
+    import itertools
+
+    rng = np.random.default_rng(7)
+    for _ in range(20):
+        size = int(rng.integers(1, 10))
+        ids = np.sort(rng.choice(100, size=size, replace=False)).astype(np.int64)
+        counts = rng.integers(1, 6, size=size).astype(np.int64)
+        lookup = dict(zip(ids.tolist(), counts.tolist()))
+        for n_hot in range(size + 1):
+            chosen = tuple(rg.top_hot(F(ids, counts), n_hot).tolist())
+            combos = list(itertools.combinations(ids.tolist(), n_hot))
+            best = max(sum(lookup[i] for i in c) for c in combos)
+            assert chosen == min(c for c in combos if sum(lookup[i] for i in c) == best)
+
+
+def _store(rg, g, owner, k=2):
+    shards = [rg.StoreShard(p, np.flatnonzero(owner == p), g.features[owner == p])
+              for p in range(k)]
+    client = rg.StoreClient(owner, [rg.InprocTransport(s) for s in shards], g.feat_dim)
+    return shards, client
+
+
+def test_bundles_match_reference(rg, plan_small, small, small_npz, golden):
+    owner = small_npz["owner2"]
+    book = rg.PartitionBook(k=2, owner=owner)
+    shards, client = _store(rg, small, owner)
+    cache, key = None, None
+    for rec in golden["bundles_small"]:
+        p = rec["part"]
+        if (p, rec["n_hot"]) != key:  # one cache per (worker, n_hot), as the golden run
+            key = (p, rec["n_hot"])
+            f0 = rg.collect_access(plan_small, book, p, epoch=0)
+            cache = (rg.build_steady(rg.top_hot(f0, rec["n_hot"]), client, rg.TransferAccount())
+                     if rec["n_hot"] else None)
+        acct = rg.TransferAccount()
+        blk = plan_small.block(0, rec["batch"])
+        b = rg.assemble_bundle(blk, owner, p, shards[p], client, cache, acct)
+        assert (b.n_local, b.n_cache_hit, b.n_fallback) == (rec["n_local"], rec["n_hit"],
+                                                           rec["n_fallback"])
+        assert list(acct.snapshot()) == rec["account"]
+        assert (cache.hits if cache else 0, cache.misses if cache else 0) == (rec["hits"],
+                                                                             rec["misses"])
+        assert np.array_equal(b.rows, small.features[blk.input_nodes])
+
+
+def _make_store(rg):
+    rng = np.random.default_rng(42)
+    feats = rng.normal(size=(10, 3)).astype(np.float32)
+    owner = (np.arange(10) % 2).astype(np.uint32)
+    shards = [rg.StoreShard(p, np.flatnonzero(owner == p), feats[owner == p]) for p in range(2)]
+    client = rg.StoreClient(owner, [rg.InprocTransport(s) for s in shards], 3)
+    return feats, owner, shards, client
+
+
+def test_store_client_semantics(rg):
+    feats, owner, shards, client = _make_store(rg)
+    ids = np.array([3, 0, 7, 2])
+    assert np.array_equal(client.sync_pull(ids), feats[ids])
+    acct = rg.TransferAccount()
+    client.vector_pull(np.array([0, 2, 4, 1]), acct)
+    assert acct.snapshot() == (2, 4, 48)
+    client.sync_pull(np.array([6]), acct)
+    assert acct.snapshot() == (3, 5, 60)
+    empty = client.sync_pull(np.empty(0, dtype=np.int64), acct)
+    assert empty.shape == (0, 3) and acct.snapshot() == (3, 5, 60)
+    assert np.array_equal(client.sync_pull(np.array([2, 2, 4])), feats[[2, 2, 4]])
+    assert np.array_equal(shards[0].rows_for_local(np.array([4, 0])), feats[[4, 0]])
+    assert shards[0].rpc_calls >= 1 and shards[1].nodes_served >= 1
+    bad = rg.StoreClient(np.zeros_like(owner), [rg.InprocTransport(s) for s in shards], 3)
+    with pytest.raises(rg.LookupError_):
+        bad.sync_pull(np.array([1]))
+
+
+def test_feature_cache_semantics(rg):
+    rng = np.random.default_rng(3)
+    feats = rng.normal(size=(40, 4)).astype(np.float32)
+    owner = np.zeros(40, dtype=np.uint32)
+    shard = rg.StoreShard(0, np.arange(40), feats)
+    client = rg.StoreClient(owner, [rg.InprocTransport(shard)], 4)
+    cache = rg.build_steady(np.array([2, 5, 9]), client)
+    res = cache.lookup(np.array([5, 1, 9, 30]))
+    assert res.found_pos.tolist() == [0, 2] and res.missing_pos.tolist() == [1, 3]
+    assert res.missing_ids.tolist() == [1, 30]
+    assert np.array_equal(res.found_rows, feats[[5, 9]])
+    assert (cache.hits, cache.misses) == (2, 2)
+    empty = rg.build_steady(np.empty(0, dtype=np.int64), client)
+    assert empty.lookup(np.array([1, 2])).missing_ids.tolist() == [1, 2]
+    c4 = rg.build_steady(np.array([4]), client)
+    assert c4.reuse_ratio() is None
+    c4.lookup(np.array([4, 4, 6, 8]))
+    assert c4.reuse_ratio() == pytest.approx(0.5)
+    acct = rg.TransferAccount()
+    rg.build_steady(np.array([1, 2, 3, 4, 5]), client, acct)
+    assert acct.snapshot() == (1, 5, 80)
+
+
+def test_double_buffer_swap(rg, plan_small, small, small_npz):
+    owner = small_npz["owner2"]
+    book = rg.PartitionBook(k=2, owner=owner)
+    shards, client = _store(rg, small, owner)
+    cache = rg.build_steady(rg.top_hot(rg.collect_access(plan_small, book, 0, epoch=0), 30),
+                            client)
+    cache.lookup(np.array([0, 5]))
+    cache.start_secondary_build(plan_small, 1, book, 0, 30, client)
+    cache.wait_secondary()
+    assert cache.swap() is True
+    expected = rg.top_hot(rg.collect_access(plan_small, book, 0, epoch=1), 30)
+    assert np.array_equal(cache.hot_ids, expected)
+    assert (cache.hits, cache.misses) == (0, 0)
+    assert np.array_equal(cache.lookup(expected).found_rows, small.features[expected])
+    assert cache.swap() is False
+
+    class Boom:
+        feat_dim = small.feat_dim
+
+        def vector_pull(self, ids, account=None):
+            raise ConnectionError("injected")
+
+    before = cache.hot_ids.copy()
+    cache.start_secondary_build(plan_small, 2, book, 0, 10, Boom())
+    cache.wait_secondary()
+    assert cache.swap() is False and np.array_equal(cache.hot_ids, before)
+
+
+def test_prefetcher_contract(rg, plan_small, small, small_npz):
+    owner = small_npz["owner2"]
+    shards, client = _store(rg, small, owner)
+    pf = rg.Prefetcher(plan_small, 0, owner, 0, shards[0], client, None, None, depth=3)
+    seen, i = [], 0
+    while (b := pf.next_bundle()) is not None:
+        ref = rg.assemble_bundle(plan_small.block(0, i), owner, 0, shards[0], client, None, None)
+        assert np.array_equal(b.rows, ref.rows)
+        seen.append(b.batch)
+        i += 1
+    assert seen == list(range(plan_small.num_batches(0)))
+    assert pf.next_bundle() is None
+    pf = rg.Prefetcher(plan_small, 0, owner, 0, shards[0], client, None, None, depth=2,
+                       start_batch=2)
+    assert pf.next_bundle().batch == 2
+    pf.drain()
+    pf.drain()
+    assert pf.next_bundle() is None
+    with pytest.raises(ValueError):
+        rg.Prefetcher(plan_small, 0, owner, 0, shards[0], client, None, None, depth=0)
+
+    class Boom:
+        def sync_pull(self, ids, account=None):
+            raise ConnectionError("injected")
+
+    pf = rg.Prefetcher(plan_small, 0, owner, 0, shards[0], Boom(), None, None, depth=2)
+    with pytest.raises(rg.PrefetchError) as exc:
+        while pf.next_bundle() is not None:
+            pass
+    assert exc.value.batch == 0
+    pf.drain()
+
+
+def test_prefetcher_bounded_runahead(rg, plan_small, small, small_npz):
+    import time
+
+    owner = small_npz["owner2"]
+    shards, client = _store(rg, small, owner)
+    pf = rg.Prefetcher(plan_small, 0, owner, 0, shards[0], client, None, None, depth=2)
+    deadline = time.monotonic() + 5
+    while pf.assembled < 3 and time.monotonic() < deadline:
+        time.sleep(0.01)
+    time.sleep(0.3)
+    assert pf.assembled <= 3  # queue depth 2 + the bundle in the producer's hand
+    pf.drain()
+
+
+def _records_equal(got, want):
+    for p, rec in enumerate(want):
+        g = got[p]["records"]
+        for e, w in enumerate(rec["epochs"]):
+            r = g[e]
+            assert [r["rpc_calls"], r["nodes_pulled"], r["bytes_pulled"], r["cache_hits"],
+                    r["cache_misses"]] == w[:5], (p, e)
+            assert r["reuse_ratio"] == w[5], (p, e)
+        assert got[p]["fill"] == rec["fill"], p
+
+
+@pytest.mark.parametrize("label", ["rapid", "baseline", "hot0", "hot1", "hot5", "global"])
+def test_replay_accounting_matches_reference_runs(rg, golden, label):
+    """The pinned REPLAY config through the device data path: every
+    per-worker per-epoch accounting column of the reference run."""
+    from paper_2505_10806_b200.pipeline import run_accounting
+
+    cfg = golden["replay"]["config"]
+    g = rg.synth_powerlaw(cfg["gen_nodes"], cfg["gen_edges_per_node"], cfg["feat_dim"],
+                          cfg["num_classes"], cfg["s0"])
+    book = rg.partition_edgecut(g, cfg["partitions"])
+    kw = {"rapid": {}, "baseline": {"mode": "baseline"}, "hot0": {"n_hot": 0},
+          "hot1": {"n_hot_pct": 1.0}, "hot5": {"n_hot_pct": 5.0},
+          "global": {"hot_scope": "global"}}[label]
+    got = run_accounting(g, book, cfg["fanouts"], cfg["batch_size"], cfg["epochs"], cfg["s0"],
+                         **kw)
+    _records_equal(got, golden["replay"][label])
+    if label in ("rapid", "baseline"):
+        per_epoch = [sum(got[p]["records"][e]["nodes_pulled"] for p in got) for e in range(5)]
+        assert per_epoch == ([326975, 326783, 326665, 326985, 327409] if label == "rapid"
+                             else [406701, 406553, 406308, 406717, 407090])
+
+
+@pytest.mark.parametrize("label", ["rapid", "baseline"])
+def test_c1_accounting_matches_reference_runs(rg, golden, label):
+    from paper_2505_10806_b200.pipeline import run_accounting
+
+    cfg = golden["c1"]["config"]
+    g = rg.synth_powerlaw(cfg["gen_nodes"], cfg["gen_edges_per_node"], cfg["feat_dim"],
+                          cfg["num_classes"], cfg["s0"])
+    book = rg.partition_edgecut(g, cfg["partitions"])
+    got = run_accounting(g, book, cfg["fanouts"], cfg["batch_size"], cfg["epochs"], cfg["s0"],
+                         mode=label)
+    _records_equal(got, golden["c1"][label])
+
+
+def test_star_marginal_uniformity(rg):
+    """Each leaf of a degree-20 star is picked equally often (test_sampler.py:146-153)."""
+    from scipy import stats
+
+    from paper_2505_10806_b200.engine import BlockSampler, DeviceGraph
+
+    g = fixture_graph("star")
+    G = 4000
+    smp = BlockSampler(DeviceGraph.of(g), [5], 1, group=G)
+    smp.seeds.zero_()
+    smp.nseeds.fill_(1)
+    seeds = np.arange(G, dtype=np.uint64)
+    smp.rng.copy_(torch.from_numpy(seeds.view(np.int64)))
+    smp.run(G)
+    picks = smp.ell[0][:, :5].cpu().numpy()
+    assert (smp.cnt[0][:, 0].cpu().numpy() == 5).all()
+    counts = np.bincount(picks.ravel() - 1, minlength=20)
+    assert stats.chisquare(counts)[1] > 0.01
+    # and the device draws equal the oracle's for a few seeds
+    for s in (0, 1, 77, 3999):
+        fr, ed = orc.block(g.indptr, g.indices, [0], [5], s)
+        assert np.array_equal(np.sort(picks[s]), ed[0][0])
