@@ -27,6 +27,7 @@ constexpr int kSlowCap = 4096;            // largest take handled (fanout cap)
 constexpr int kCompactWords = 1024;       // bitmap words per compaction CTA
 constexpr int kCompactThreads = 256;
 constexpr int kScanElems = 1024;          // elements per ELL-scan CTA
+constexpr int kMaxGroupSeeds = 64;        // batches whose step seed is kept in smem
 
 __device__ __forceinline__ void mark(uint32_t* bm, int32_t v) {
   atomicOr(bm + (v >> 5), 1u << (v & 31));
@@ -137,9 +138,9 @@ __device__ __forceinline__ bool select_threshold(uint64_t nk, int D, int T, uint
                                                  int32_t* s_pos, int& pos_out) {
   const int lane = lane_id();
   const unsigned lt = (1u << lane) - 1u;
-  const double mu = (double)T + 3.0 * sqrt((double)T) + 3.0;
-  const double frac = mu / (double)D;
-  const uint64_t t0 = frac >= 1.0 ? ~0ull : (uint64_t)(frac * 18446744073709551616.0);
+  const float mu = (float)T + 3.0f * sqrtf((float)T) + 3.0f;
+  const float frac = mu / (float)D;  // approximate is fine: only the candidate count moves
+  const uint64_t t0 = frac >= 1.0f ? ~0ull : (uint64_t)(frac * 18446744073709551616.0f);
   int count = 0;
   uint64_t kk = nk + (uint64_t)(lane + 1) * GOLDEN;
   const uint64_t step = 32ull * GOLDEN;
@@ -185,9 +186,16 @@ __global__ void __launch_bounds__(kSampleWarps * 32)
   __shared__ int s_next;
   __shared__ uint64_t s_key[kSampleWarps][64];
   __shared__ int32_t s_pos[kSampleWarps][96];
+  __shared__ uint64_t s_seed[kMaxGroupSeeds];  // step seed s_d per batch
+  __shared__ int s_nf[kMaxGroupSeeds];
   const int lane = lane_id();
   const int warp = threadIdx.x >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
+  const bool seeds_in_smem = G <= kMaxGroupSeeds;
+  for (int b = threadIdx.x; b < G && seeds_in_smem; b += blockDim.x) {
+    s_seed[b] = mix64(rng_seed[b] ^ level_mix);
+    s_nf[b] = nfront[b];
+  }
   int maxf = 0;
   for (int b = lane; b < G; b += 32) maxf = max(maxf, nfront[b]);
 #pragma unroll
@@ -197,16 +205,17 @@ __global__ void __launch_bounds__(kSampleWarps * 32)
   // items k = j*G + b, interleaved so the low (hub-heavy) frontier ranks of
   // every batch are spread over all CTAs; CTA c owns k = c, c + grid, ...
   // and its warps pull them dynamically through a shared counter.
-  const int64_t total = (int64_t)maxf * G;
-  const int64_t grid = gridDim.x;
+  // (G * max|F| < 2^31: 32-bit index math.)
+  const unsigned total = (unsigned)maxf * (unsigned)G;
+  const unsigned grid = gridDim.x;
   for (;;) {
     int t = 0;
     if (lane == 0) t = atomicAdd(&s_next, 1);
     t = __shfl_sync(kFull, t, 0);
-    const int64_t k = blockIdx.x + (int64_t)t * grid;
+    const unsigned k = blockIdx.x + (unsigned)t * grid;
     if (k >= total) break;
-    const int j = (int)(k / G), b = (int)(k - (int64_t)j * G);
-    if (j >= nfront[b]) continue;
+    const int j = (int)(k / (unsigned)G), b = (int)(k - (unsigned)j * (unsigned)G);
+    if (j >= (seeds_in_smem ? s_nf[b] : nfront[b])) continue;
     const int64_t row = (int64_t)b * cap_in + j;
     const int32_t v = front[row];
     const int64_t a = indptr[v];
@@ -228,7 +237,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32)
       if (D <= F) {
         sel = D == 32 ? kFull : ((1u << D) - 1u);
       } else {
-        const uint64_t sd = mix64(rng_seed[b] ^ level_mix);
+        const uint64_t sd = seeds_in_smem ? s_seed[b] : mix64(rng_seed[b] ^ level_mix);
         const uint64_t nk = mix64(((uint64_t)v + 1ull) * GOLDEN ^ sd);
         const uint64_t key = lane < D ? mix64(nk + (uint64_t)(lane + 1) * GOLDEN) : ~0ull;
         sel = select_mask32(key, __ballot_sync(kFull, lane < D), T);
@@ -251,7 +260,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32)
       continue;
     }
     // D > 32 (> F): threshold candidates, else the running top-T list
-    const uint64_t sd = mix64(rng_seed[b] ^ level_mix);
+    const uint64_t sd = seeds_in_smem ? s_seed[b] : mix64(rng_seed[b] ^ level_mix);
     const uint64_t nk = mix64(((uint64_t)v + 1ull) * GOLDEN ^ sd);
     int pos;
     const bool ordered = select_threshold(nk, D, T, s_key[warp], s_pos[warp], pos);
