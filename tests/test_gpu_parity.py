@@ -394,3 +394,32 @@ def test_star_marginal_uniformity(rg):
     for s in (0, 1, 77, 3999):
         fr, ed = orc.block(g.indptr, g.indices, [0], [5], s)
         assert np.array_equal(np.sort(picks[s]), ed[0][0])
+
+
+def test_sage_mean_fwd_bwd_bit_exact(rg):
+    """K8 against the reference's in-order numpy semantics (model.py:72-81, 126-135)."""
+    from paper_2505_10806_b200.aggregate import edges_to_ell, sage_mean, sage_mean_backward
+
+    g = rg.synth_powerlaw(20000, 5, 64, 8, seed=7)
+    rng = np.random.default_rng(11)
+    blk = rg.sample_block(g, rng.choice(20000, 256, replace=False), [10, 25], 99)
+    h0 = g.features[blk.input_nodes]
+    for d in range(blk.num_layers - 1, -1, -1):
+        src_front, dst_front = blk.frontiers[d + 1], blk.frontiers[d]
+        src, dst = blk.edges[d]
+        h = h0 if d == blk.num_layers - 1 else rng.standard_normal(
+            (len(src_front), 48)).astype(np.float32)
+        want_mean, want_self = orc.mean_aggregate(h, src_front, dst_front, src, dst)
+        ell, cnt, F = edges_to_ell(dst_front, src, dst)
+        dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+        mean, hself, self_pos = sage_mean(dev(h), dev(src_front.astype(np.int32)),
+                                          dev(dst_front.astype(np.int32)), dev(ell), dev(cnt), F)
+        assert np.array_equal(mean.cpu().numpy(), want_mean)
+        assert np.array_equal(hself.cpu().numpy(), want_self)
+        dself = rng.standard_normal(want_mean.shape).astype(np.float32)
+        dmean = rng.standard_normal(want_mean.shape).astype(np.float32)
+        want_dh = orc.mean_aggregate_bwd(dself, dmean, len(src_front), src_front, dst_front,
+                                         src, dst)
+        dh = sage_mean_backward(dev(dself), dev(dmean), dev(cnt), self_pos,
+                                dev(src_front.astype(np.int32)), dev(ell), F)
+        assert np.array_equal(dh.cpu().numpy(), want_dh)
