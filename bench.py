@@ -266,7 +266,7 @@ def main():
     shard_ids = [np.flatnonzero(owner == q) for q in range(k)]
     for q in range(k):
         if q % world == rank:
-            store.set_shard(q, FeatureStore.pad_rows(g.features[shard_ids[q]], store.stride,
+            store.set_shard(q, FeatureStore.pad_rows(g.features[shard_ids[q]], store.src_stride,
                                                      dg.device))
     if world > 1:
         multigpu.exchange_shards(store, rank, world)

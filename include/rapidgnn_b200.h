@@ -147,16 +147,19 @@ int rg_route_with_cache(const uint32_t* d_base_route, int64_t n, const int32_t* 
 
 /* Feature bundle gather for G batches (prefetch.py:41-88, cache.py:54-78,
  * store.py:66-69,173-196).  Row j of batch b is copied bit-exactly from
- *   bases[kind] + (route[id] & RG_ROW_MASK) * stride
- * to out[(b*cap + j) * stride], kind = route >> 28 (partition shard or
- * cache).  Classification per row: kind == my_part -> local, kind ==
- * RG_KIND_CACHE -> cache hit, else fallback pull from shard `kind`.
- * d_counters: G x RG_NCOUNTERS uint32, accumulated (caller zeroes).
- * h_bases: host array of 16 device pointers (peer pointers allowed);
- * stride = row stride in floats, multiple of 4 (16-byte rows).        */
+ *   bases[kind] + (route[id] & RG_ROW_MASK) * src_stride
+ * to out[(b*cap + j) * stride] (stride floats), kind = route >> 28
+ * (partition shard or cache).  Classification per row: kind == my_part ->
+ * local, kind == RG_KIND_CACHE -> cache hit, else fallback pull from shard
+ * `kind`.  d_counters: G x RG_NCOUNTERS uint32, accumulated (caller zeroes).
+ * h_bases: host array of 16 device pointers (peer pointers allowed).
+ * stride, src_stride: floats, multiples of 4 (16-byte rows); src_stride >=
+ * stride lets sources keep sector/line-aligned padded rows (NVLink reads
+ * run at full rate on 128-byte-aligned rows) while the bundle stays dense. */
 int rg_gather_bundle(const int32_t* d_ids, const int32_t* d_nids, int64_t cap, int32_t G,
-                     const uint32_t* d_route, const float* const* h_bases, int32_t stride,
-                     int32_t my_part, float* d_out, uint32_t* d_counters, void* stream);
+                     const uint32_t* d_route, const float* const* h_bases, int32_t src_stride,
+                     int32_t stride, int32_t my_part, float* d_out, uint32_t* d_counters,
+                     void* stream);
 
 /* ---- L5 aggregation consumer (model.py:72-81, 126-135) -------------- */
 /* mean[t] = (sum over t's edges, in stored order, of h[pos(src)]) /
@@ -198,6 +201,8 @@ int rg_partition_edgecut(int64_t n, const int64_t* h_indptr, const int32_t* h_in
 int rg_ipc_handle(const void* d_ptr, uint8_t* h_handle64, int64_t* h_offset);
 int rg_ipc_open(const uint8_t* h_handle64, void** d_ptr_out);
 int rg_ipc_close(void* d_ptr);
+/* single process, several GPUs: current device may read `peer`'s memory  */
+int rg_enable_peer(int32_t peer);
 
 #ifdef __cplusplus
 }

@@ -53,7 +53,8 @@ _SIGNATURES = {
     "rg_threshold_split": (c_int32, [P, P, c_int64, c_uint32, P, P, P]),
     "rg_gather_counts": (c_int32, [P, P, P, c_int64, P, P]),
     "rg_route_with_cache": (c_int32, [P, c_int64, P, c_int64, P, P]),
-    "rg_gather_bundle": (c_int32, [P, P, c_int64, c_int32, P, P, c_int32, c_int32, P, P, P]),
+    "rg_gather_bundle": (c_int32, [P, P, c_int64, c_int32, P, P, c_int32, c_int32, c_int32, P, P,
+                                   P]),
     "rg_sage_mean_fwd": (c_int32, [P, c_int64, c_int32, c_int32, P, P, c_int64, P, P, c_int32, P,
                                    P, P, P]),
     "rg_sage_transpose_scratch": (c_int64, [c_int64, c_int64, c_int32]),
@@ -65,6 +66,7 @@ _SIGNATURES = {
     "rg_ipc_handle": (c_int32, [P, P, P]),
     "rg_ipc_open": (c_int32, [P, ctypes.POINTER(c_void_p)]),
     "rg_ipc_close": (c_int32, [P]),
+    "rg_enable_peer": (c_int32, [c_int32]),
 }
 
 _lock = threading.Lock()

@@ -102,3 +102,23 @@ extern "C" int rg_ipc_close(void* d_ptr) {
   }
   return RG_OK;
 }
+
+// single-process multi-GPU: let the current device read `peer`'s memory
+extern "C" int rg_enable_peer(int32_t peer) {
+  int cur = 0, can = 0;
+  cudaGetDevice(&cur);
+  if (cudaDeviceCanAccessPeer(&can, cur, peer) != cudaSuccess || !can) {
+    rg::set_error("device %d cannot access peer %d", cur, peer);
+    return RG_ERR_UNSUPPORTED;
+  }
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return RG_OK;
+  }
+  if (e != cudaSuccess) {
+    rg::set_error("cudaDeviceEnablePeerAccess: %s", cudaGetErrorString(e));
+    return RG_ERR_CUDA;
+  }
+  return RG_OK;
+}

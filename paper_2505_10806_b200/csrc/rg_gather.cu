@@ -28,7 +28,7 @@ struct Bases {
 __global__ void __launch_bounds__(kGatherWarps * 32)
     gather_bundle_kernel(const int32_t* __restrict__ ids, const int32_t* __restrict__ nids,
                          int64_t cap, const uint32_t* __restrict__ route, const __grid_constant__ Bases bases,
-                         int stride, int nvec, int dq, int dr, int my_part,
+                         int src_stride, int stride, int nvec, int dq, int dr, int my_part,
                          float* __restrict__ out, uint32_t* __restrict__ counters) {
   __shared__ uint32_t s_cnt[RG_NCOUNTERS];
   __shared__ const float* s_base[16];
@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(kGatherWarps * 32)
     c_bad += __popc(__ballot_sync(kFull, bad));
     omask |= __reduce_or_sync(kFull, fb ? (1u << kind) : 0u);
     const float* src = nullptr;
-    if (bp) src = bp + (int64_t)(rt & RG_ROW_MASK) * stride;
+    if (bp) src = bp + (int64_t)(rt & RG_ROW_MASK) * src_stride;
     const unsigned long long srcu = reinterpret_cast<unsigned long long>(src);
     float4* dst = reinterpret_cast<float4*>(out + ((int64_t)b * cap + r0) * stride);
     const int total = nr * nvec;
@@ -143,10 +143,13 @@ using namespace rg;
 
 extern "C" int rg_gather_bundle(const int32_t* d_ids, const int32_t* d_nids, int64_t cap,
                                 int32_t G, const uint32_t* d_route, const float* const* h_bases,
-                                int32_t stride, int32_t my_part, float* d_out,
+                                int32_t src_stride, int32_t stride, int32_t my_part, float* d_out,
                                 uint32_t* d_counters, void* stream) {
   RG_REQUIRE(G >= 1 && G <= 65535 && cap >= 1, "rg_gather_bundle: bad sizes");
   RG_REQUIRE(stride >= 4 && stride % 4 == 0, "rg_gather_bundle: stride %d not a multiple of 4",
+             stride);
+  RG_REQUIRE(src_stride >= stride && src_stride % 4 == 0,
+             "rg_gather_bundle: src_stride %d < stride %d or not a multiple of 4", src_stride,
              stride);
   RG_REQUIRE(((uintptr_t)d_out & 15) == 0, "rg_gather_bundle: output not 16-byte aligned");
   Bases bases;
@@ -156,6 +159,7 @@ extern "C" int rg_gather_bundle(const int32_t* d_ids, const int32_t* d_nids, int
   }
   const int nvec = stride / 4;
   const int dq = 32 / nvec, dr = 32 % nvec;
+
   // enough CTAs for ~4 resident per SM on the largest slot; extra CTAs of a
   // short batch exit after one bounds check.
   static const int ctas_per_sm = [] {
@@ -166,7 +170,8 @@ extern "C" int rg_gather_bundle(const int32_t* d_ids, const int32_t* d_nids, int
   const int gx = (int)std::max<int64_t>(
       1, std::min<int64_t>(want, ((int64_t)kNumSMs * ctas_per_sm + G - 1) / G));
   gather_bundle_kernel<<<dim3(gx, G), kGatherWarps * 32, 0, (cudaStream_t)stream>>>(
-      d_ids, d_nids, cap, d_route, bases, stride, nvec, dq, dr, my_part, d_out, d_counters);
+      d_ids, d_nids, cap, d_route, bases, src_stride, stride, nvec, dq, dr, my_part, d_out,
+      d_counters);
   return check_launch("gather_bundle");
 }
 

@@ -27,7 +27,21 @@ I32 = torch.int32
 
 
 def stride_for(d: int) -> int:
+    """Dense row stride (floats) of bundles: d rounded up to 16 bytes."""
     return max(4, (d + 3) // 4 * 4)
+
+
+# Shard/cache row alignment.  Measured (tools/nvlink_probe.py, round 1):
+# 128-byte-aligned 400-B rows gained only +1-2 % on local and peer gathers and
+# lost 1 % in the full bench, so rows stay dense (16-byte aligned); the
+# separate source stride remains available.
+SRC_ALIGN_FLOATS = 4
+
+
+def src_stride_for(d: int) -> int:
+    """Row stride (floats) of shards and cache rows."""
+    a = SRC_ALIGN_FLOATS
+    return max(4, (d + a - 1) // a * a)
 
 
 def _cur() -> int:
@@ -199,7 +213,8 @@ class FeatureStore:
         self.device = torch.device(device or "cuda")
         self.k = int(num_parts)
         self.d = int(feat_dim)
-        self.stride = stride_for(self.d)
+        self.stride = stride_for(self.d)  # bundle rows
+        self.src_stride = src_stride_for(self.d)  # shard / cache rows
         self.owner_np = np.asarray(owner)
         self.n = len(self.owner_np)
         self.owner = torch.from_numpy(self.owner_np.astype(np.uint8)).to(self.device)
@@ -230,20 +245,23 @@ def bases_array(bases) -> np.ndarray:
 
 
 def gather_bundle(ids: torch.Tensor, nids: torch.Tensor, cap: int, G: int, route: torch.Tensor,
-                  bases: np.ndarray, stride: int, my_part: int, out: torch.Tensor,
-                  counters: torch.Tensor) -> None:
+                  bases: np.ndarray, src_stride: int, stride: int, my_part: int,
+                  out: torch.Tensor, counters: torch.Tensor) -> None:
     """rg_gather_bundle on the current stream (bases: host uint64[16])."""
     _lib.call("rg_gather_bundle", ptr(ids), ptr(nids), cap, G, ptr(route), bases.ctypes.data,
-              stride, my_part, ptr(out), ptr(counters), _cur())
+              src_stride, stride, my_part, ptr(out), ptr(counters), _cur())
 
 
-def gather_rows(base: torch.Tensor, row_idx: np.ndarray | torch.Tensor, stride: int) -> torch.Tensor:
-    """out[i] = base[row_idx[i]] via the bundle kernel with an identity route."""
+def gather_rows(base: torch.Tensor, row_idx: np.ndarray | torch.Tensor, stride: int,
+                out_stride: int | None = None) -> torch.Tensor:
+    """out[i] = base[row_idx[i]] (base rows of `stride` floats) via the bundle
+    kernel with an identity route; out rows have out_stride <= stride floats."""
+    out_stride = stride if out_stride is None else out_stride
     dev = base.device
     idx = (torch.from_numpy(np.ascontiguousarray(row_idx, dtype=np.int32)).to(dev)
            if isinstance(row_idx, np.ndarray) else row_idx.to(torch.int32))
     n = int(idx.numel())
-    out = torch.empty((max(n, 1), stride), dtype=torch.float32, device=dev)
+    out = torch.empty((max(n, 1), out_stride), dtype=torch.float32, device=dev)
     if n == 0:
         return out[:0]
     # route: kind 0 | row index, ids 0..n-1 index the route directly
@@ -252,5 +270,5 @@ def gather_rows(base: torch.Tensor, row_idx: np.ndarray | torch.Tensor, stride: 
     nids = torch.tensor([n], dtype=I32, device=dev)
     bases = bases_array([base.data_ptr()])
     counters = torch.zeros((1, _lib.RG_NCOUNTERS), dtype=I32, device=dev)
-    gather_bundle(ids, nids, n, 1, route, bases, stride, 0, out, counters)
+    gather_bundle(ids, nids, n, 1, route, bases, stride, out_stride, 0, out, counters)
     return out

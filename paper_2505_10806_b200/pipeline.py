@@ -92,14 +92,16 @@ class WorkerPipeline:
         """VectorPull of the hot rows + cache route (cache.py:139-148)."""
         st = self.store
         n_hot = int(hot_ids.numel())
-        rows = torch.empty((max(n_hot, 1), st.stride), dtype=torch.float32, device=self.dg.device)
+        rows = torch.empty((max(n_hot, 1), st.src_stride), dtype=torch.float32,
+                           device=self.dg.device)
         route = torch.empty_like(st.route)
         cnt = torch.zeros((1, _lib.RG_NCOUNTERS), dtype=I32, device=self.dg.device)
         s = _lib.stream_handle()
         if n_hot:
             nids = torch.tensor([n_hot], dtype=I32, device=self.dg.device)
             _lib.call("rg_gather_bundle", ptr(hot_ids), ptr(nids), n_hot, 1, ptr(st.route),
-                      bases_array(st.bases).ctypes.data, st.stride, -1, ptr(rows), ptr(cnt), s)
+                      bases_array(st.bases).ctypes.data, st.src_stride, st.src_stride, -1,
+                      ptr(rows), ptr(cnt), s)
         _lib.call("rg_route_with_cache", ptr(st.route), st.n, ptr(hot_ids), n_hot, ptr(route), s)
         c = cnt.cpu().numpy()[0].view(np.uint32)
         rpcs = bin(int(c[_lib.RG_CNT_OWNER_MASK])).count("1")
@@ -163,7 +165,8 @@ class WorkerPipeline:
             bases[_lib.RG_KIND_CACHE] = self.cache.rows.data_ptr()
             route = self.cache.route
         _lib.call("rg_gather_bundle", ptr(smp.front[smp.L]), ptr(smp.nfront[smp.L]), self.cap_in,
-                  ng, ptr(route), bases_array(bases).ctypes.data, st.stride, self.my_part,
+                  ng, ptr(route), bases_array(bases).ctypes.data, st.src_stride, st.stride,
+                  self.my_part,
                   ptr(rows), ptr(self.counters) + i0 * _lib.RG_NCOUNTERS * 4,
                   _lib.stream_handle())
 
@@ -204,7 +207,7 @@ def run_accounting(g, book, fanouts, batch_size: int, epochs: int, s0: int, mode
     for q in range(k):
         rows = (g.features[shard_ids[q]] if features
                 else np.zeros((len(shard_ids[q]), d), dtype=np.float32))
-        store.set_shard(q, FeatureStore.pad_rows(rows, store.stride, dg.device))
+        store.set_shard(q, FeatureStore.pad_rows(rows, store.src_stride, dg.device))
     store.build_route(shard_ids)
     train = np.flatnonzero(g.train_mask)
     workers = list(range(k)) if workers is None else list(workers)

@@ -19,7 +19,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from .engine import FeatureStore, bases_array, gather_bundle, gather_rows, route_table, stride_for
+from .engine import (FeatureStore, bases_array, gather_bundle, gather_rows, route_table,
+                     src_stride_for, stride_for)
 
 
 class LookupError_(KeyError):
@@ -63,10 +64,11 @@ class StoreShard:
         self.owned_ids = np.asarray(owned_ids, dtype=np.int64)
         rows = np.ascontiguousarray(rows, dtype=np.float32)
         self.feat_dim = rows.shape[1] if rows.ndim == 2 else 0
-        self.stride = stride_for(self.feat_dim)
+        self.stride = stride_for(self.feat_dim)  # dense rows handed out
+        self.src_stride = src_stride_for(self.feat_dim)  # line-aligned rows in HBM
         self.device = torch.device(device or "cuda")
         self.rows_device = FeatureStore.pad_rows(rows.reshape(len(self.owned_ids), -1),
-                                                 self.stride, self.device)
+                                                 self.src_stride, self.device)
         self.latency_ms = latency_ms
         self._lock = threading.Lock()
         self.rpc_calls = 0
@@ -80,7 +82,7 @@ class StoreShard:
     def rows_for_local(self, ids: np.ndarray) -> np.ndarray:
         """Direct memory read for the owning worker; no RPC, no counters."""
         pos = np.searchsorted(self.owned_ids, np.asarray(ids, dtype=np.int64))
-        out = gather_rows(self.rows_device, pos.astype(np.int32), self.stride)
+        out = gather_rows(self.rows_device, pos.astype(np.int32), self.src_stride, self.stride)
         return out[:, : self.feat_dim].cpu().numpy()
 
     def _served(self, nodes: int) -> None:
@@ -132,6 +134,7 @@ class StoreClient:
         self.transports = transports
         self.feat_dim = feat_dim
         self.stride = stride_for(feat_dim)
+        self.src_stride = src_stride_for(feat_dim)
         self.k = len(transports)
         if self.k > _lib.RG_MAX_PARTS:
             raise NotImplementedError(f"at most {_lib.RG_MAX_PARTS} shards")
@@ -143,7 +146,7 @@ class StoreClient:
         bases = []
         for s in shards:
             if isinstance(s, StoreShard):
-                if s.stride != self.stride:
+                if s.src_stride != self.src_stride:
                     raise ValueError(f"shard {s.part} has dim {s.feat_dim}, expected {feat_dim}")
                 bases.append(s.rows_device.data_ptr())
             else:
@@ -158,19 +161,22 @@ class StoreClient:
             b[_lib.RG_KIND_CACHE] = cache_rows.data_ptr()
         return bases_array(b)
 
-    def pull_device(self, ids: np.ndarray, account: TransferAccount | None):
-        """Rows for ids (device, padded stride) + provenance counters."""
+    def pull_device(self, ids: np.ndarray, account: TransferAccount | None,
+                    out_stride: int | None = None):
+        """Rows for ids (device; dense stride, or out_stride) + RPC count."""
+        out_stride = self.stride if out_stride is None else out_stride
         ids = np.asarray(ids, dtype=np.int64)
         n = len(ids)
         if n and (ids.min() < 0 or ids.max() >= len(self.owner)):
             raise LookupError_("requested id outside the graph")
-        out = torch.empty((max(n, 1), self.stride), dtype=torch.float32, device=self.device)
+        out = torch.empty((max(n, 1), out_stride), dtype=torch.float32, device=self.device)
         if n == 0:
             return out[:0], 0
         dev_ids = torch.from_numpy(ids.astype(np.int32)).to(self.device)
         nids = torch.tensor([n], dtype=torch.int32, device=self.device)
         counters = torch.zeros((1, _lib.RG_NCOUNTERS), dtype=torch.int32, device=self.device)
-        gather_bundle(dev_ids, nids, n, 1, self.route, self.bases(), self.stride, -1, out,
+        gather_bundle(dev_ids, nids, n, 1, self.route, self.bases(), self.src_stride, out_stride,
+                      -1, out,
                       counters)
         c = counters.cpu().numpy()[0].view(np.uint32)
         if c[_lib.RG_CNT_BAD]:
