@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--config", default="products", choices=sorted(CONFIGS))
     ap.add_argument("--group", type=int, default=32)
     ap.add_argument("--cache-pct", type=float, default=15.0)
+    ap.add_argument("--prng", default="splitmix",
+                    choices=["splitmix", "pcg32", "sfc64", "xoshiro256pp"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
@@ -273,7 +275,7 @@ def main():
     store.build_route(shard_ids)
     train = np.flatnonzero(g.train_mask)
     pipe = WorkerPipeline(dg, store, part, train, cfg["fanouts"], cfg["batch"], S0, args.group,
-                          nbuf=1 if args.serial else 2)
+                          nbuf=1 if args.serial else 2, prng=args.prng)
     nb, G = pipe.nb, pipe.G
     sched = SeedSchedule(S0, 1, nb)
 
@@ -413,6 +415,7 @@ def main():
                  f"partition_edgecut(k={k})"),
         "config": {"workload": args.config, "batch_size": cfg["batch"], "fanouts": cfg["fanouts"],
                    "partitions": k, "worker": part, "cache_pct": args.cache_pct, "n_hot": n_hot,
+                   "prng": args.prng,
                    "batches_per_step": G, "parallelism": f"worker-per-gpu x{world}",
                    "l2": "inputs larger than L2 (feature shards %.0f MB; bundle %.0f MB/batch)"
                          % (g.num_nodes * d * 4 / 1e6, float(rows_b.mean()) * d * 4 / 1e6)},

@@ -96,7 +96,19 @@ int rg_sample_level(const int64_t* d_indptr, const int32_t* d_indices, int64_t n
                     int32_t G, const int32_t* d_front, int64_t cap_in, const int32_t* d_nfront,
                     int32_t fanout, int32_t level, const uint64_t* d_rng_seed, int32_t* d_ell,
                     int32_t* d_cnt, uint32_t* d_bm, int64_t nwords, int32_t* d_slow,
-                    int32_t sorted_rows, void* stream);
+                    int32_t sorted_rows, int32_t prng, void* stream);
+
+/* PRNG variants (not in the reference; semantics in rg_prng.cuh and
+ * DESIGN.md §10): prng = 0 SplitMix64 keys (reference), 1 pcg32,
+ * 2 sfc64, 3 xoshiro256++ (passed to rg_sample_level).  Host forms for
+ * known-answer tests: raw stream seeded with (k0, k1), and the Floyd
+ * position draw of one node (positions in draw order).                 */
+#define RG_PRNG_SPLITMIX 0
+#define RG_PRNG_PCG32 1
+#define RG_PRNG_SFC64 2
+#define RG_PRNG_XOSHIRO256PP 3
+int rg_prng_raw(int32_t kind, uint64_t k0, uint64_t k1, int64_t count, uint64_t* h_out);
+int rg_prng_select(int32_t kind, uint64_t nk, uint64_t sd, int32_t D, int32_t T, int32_t* h_pos);
 
 /* Sorted-unique compaction of G bitmaps (np.unique / np.union1d).
  * Writes ascending ids of set bits to out[b*cap_out ...], count to

@@ -28,6 +28,7 @@ RG_ROUTE_INVALID = 0xFFFFFFFF
 RG_MAX_PARTS = 15
 RG_CNT_LOCAL, RG_CNT_HIT, RG_CNT_FALLBACK, RG_CNT_OWNER_MASK, RG_CNT_BAD = 0, 1, 2, 3, 4
 RG_NCOUNTERS = 8
+PRNG_KINDS = {"splitmix": 0, "pcg32": 1, "sfc64": 2, "xoshiro256pp": 3}
 
 P = c_void_p
 # name -> (restype, argtypes); mirrors include/rapidgnn_b200.h
@@ -41,7 +42,7 @@ _SIGNATURES = {
                                 c_int64, P, P]),
     "rg_mark_seeds": (c_int32, [P, P, c_int32, c_int32, P, c_int64, P]),
     "rg_sample_level": (c_int32, [P, P, c_int64, c_int32, P, c_int64, P, c_int32, c_int32, P, P,
-                                  P, P, c_int64, P, c_int32, P]),
+                                  P, P, c_int64, P, c_int32, c_int32, P]),
     "rg_bitmap_chunks": (c_int64, [c_int64]),
     "rg_bitmap_compact": (c_int32, [P, c_int64, c_int32, P, P, c_int64, P, P, P]),
     "rg_bitmap_set": (c_int32, [P, P, P, P]),
@@ -60,6 +61,8 @@ _SIGNATURES = {
     "rg_sage_transpose_scratch": (c_int64, [c_int64, c_int64, c_int32]),
     "rg_sage_transpose": (c_int32, [P, c_int64, P, P, c_int64, c_int32, P, P, P, P]),
     "rg_sage_mean_bwd": (c_int32, [P, P, c_int64, c_int32, P, P, P, P, c_int64, P, P, P]),
+    "rg_prng_raw": (c_int32, [c_int32, c_uint64, c_uint64, c_int64, P]),
+    "rg_prng_select": (c_int32, [c_int32, c_uint64, c_uint64, c_int32, c_int32, P]),
     "rg_philox_raw": (c_int32, [c_uint64, c_uint64, c_int64, P]),
     "rg_synth_powerlaw_csr": (c_int32, [c_int64, c_int64, c_uint64, c_uint64, P, P, P]),
     "rg_partition_edgecut": (c_int32, [c_int64, P, P, c_int32, P]),

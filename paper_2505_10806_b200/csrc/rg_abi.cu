@@ -4,6 +4,7 @@
 #include <cstring>
 
 #include "rg_common.cuh"
+#include "rg_prng.cuh"
 
 namespace rg {
 
@@ -119,6 +120,58 @@ extern "C" int rg_enable_peer(int32_t peer) {
   if (e != cudaSuccess) {
     rg::set_error("cudaDeviceEnablePeerAccess: %s", cudaGetErrorString(e));
     return RG_ERR_CUDA;
+  }
+  return RG_OK;
+}
+
+// host forms of the PRNG variants (for known-answer tests against the oracle)
+extern "C" int rg_prng_raw(int32_t kind, uint64_t k0, uint64_t k1, int64_t count, uint64_t* out) {
+  using namespace rg;
+  if (count < 0) return RG_ERR_INVALID;
+  if (kind == kPcg32) {
+    Pcg32 g;
+    g.seed(k0, k1);
+    for (int64_t i = 0; i < count; ++i) out[i] = g.next32();
+  } else if (kind == kSfc64) {
+    Sfc64 g;
+    g.seed(k0, k1);
+    for (int64_t i = 0; i < count; ++i) out[i] = g.next64();
+  } else if (kind == kXoshiro256pp) {
+    Xoshiro256pp g;
+    g.seed(k0, k1);
+    for (int64_t i = 0; i < count; ++i) out[i] = g.next64();
+  } else {
+    set_error("rg_prng_raw: unknown kind %d", kind);
+    return RG_ERR_INVALID;
+  }
+  return RG_OK;
+}
+
+extern "C" int rg_prng_select(int32_t kind, uint64_t nk, uint64_t sd, int32_t D, int32_t T,
+                              int32_t* pos) {
+  using namespace rg;
+  if (D < 0 || T < 0 || T > D) return RG_ERR_INVALID;
+  Pcg32 g1;
+  Sfc64 g2;
+  Xoshiro256pp g3;
+  g1.seed(nk, sd);
+  g2.seed(nk, sd);
+  g3.seed(nk, sd);
+  int n = 0;
+  for (int j = D - T; j < D; ++j) {
+    const uint32_t m = (uint32_t)(j + 1);
+    int t;
+    if (kind == kPcg32)
+      t = (int)g1.bounded(m);
+    else if (kind == kSfc64)
+      t = (int)g2.bounded(m);
+    else if (kind == kXoshiro256pp)
+      t = (int)g3.bounded(m);
+    else
+      return RG_ERR_INVALID;
+    bool dup = false;
+    for (int i = 0; i < n; ++i) dup |= pos[i] == t;
+    pos[n++] = dup ? j : t;
   }
   return RG_OK;
 }

@@ -18,6 +18,7 @@
 #include <climits>
 
 #include "rg_common.cuh"
+#include "rg_prng.cuh"
 
 namespace rg {
 namespace {
@@ -28,6 +29,7 @@ constexpr int kCompactWords = 1024;       // bitmap words per compaction CTA
 constexpr int kCompactThreads = 256;
 constexpr int kScanElems = 1024;          // elements per ELL-scan CTA
 constexpr int kMaxGroupSeeds = 64;        // batches whose step seed is kept in smem
+constexpr int kFloydBits = 65536;         // PRNG slow path: largest degree with fanout > 32
 
 __device__ __forceinline__ void mark(uint32_t* bm, int32_t v) {
   atomicOr(bm + (v >> 5), 1u << (v & 31));
@@ -176,13 +178,44 @@ __device__ __forceinline__ bool select_threshold(uint64_t nk, int D, int T, uint
   return true;
 }
 
+// PRNG-variant selection (rg_prng.cuh): Floyd's algorithm with the
+// generator replicated in every lane (warp-uniform draws); lane r < T ends
+// with the r-th drawn position (unsorted).
+template <typename Gen>
+__device__ __forceinline__ int floyd_positions(Gen& g, int D, int T) {
+  const int lane = lane_id();
+  int mine = -1;
+  for (int j = D - T, n = 0; j < D; ++j, ++n) {
+    const int t = (int)g.bounded((uint32_t)(j + 1));
+    const bool dup = __ballot_sync(kFull, lane < n && mine == t) != 0u;
+    if (lane == n) mine = dup ? j : t;
+  }
+  return mine;
+}
+
+__device__ __forceinline__ int prng_positions(int prng, uint64_t nk, uint64_t sd, int D, int T) {
+  if (prng == kPcg32) {
+    Pcg32 g;
+    g.seed(nk, sd);
+    return floyd_positions(g, D, T);
+  }
+  if (prng == kSfc64) {
+    Sfc64 g;
+    g.seed(nk, sd);
+    return floyd_positions(g, D, T);
+  }
+  Xoshiro256pp g;
+  g.seed(nk, sd);
+  return floyd_positions(g, D, T);
+}
+
 __global__ void __launch_bounds__(kSampleWarps * 32)
     sample_level_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                         int G, const int32_t* __restrict__ front, int64_t cap_in,
                         const int32_t* __restrict__ nfront, int F, uint64_t level_mix,
                         const uint64_t* __restrict__ rng_seed, int32_t* __restrict__ ell,
                         int32_t* __restrict__ cnt, uint32_t* __restrict__ bm, int64_t nwords,
-                        int32_t* __restrict__ slow, int sorted_rows) {
+                        int32_t* __restrict__ slow, int sorted_rows, int prng) {
   __shared__ int s_next;
   __shared__ uint64_t s_key[kSampleWarps][64];
   __shared__ int32_t s_pos[kSampleWarps][96];
@@ -231,6 +264,25 @@ __global__ void __launch_bounds__(kSampleWarps * 32)
     }
     int32_t* out = ell + row * F;
     uint32_t* bmb = bm + (int64_t)b * nwords;
+    if (prng != kSplitMix && D > F) {
+      const uint64_t sd = seeds_in_smem ? s_seed[b] : mix64(rng_seed[b] ^ level_mix);
+      const uint64_t nk = mix64(((uint64_t)v + 1ull) * GOLDEN ^ sd);
+      int p = prng_positions(prng, nk, sd, D, T);
+      int32_t x = INT_MAX;
+      if (sorted_rows) {
+        if (lane >= T) p = INT_MAX;
+        warp_bitonic_sort_keys(p);
+        if (lane < T) x = __ldg(indices + a + p);
+      } else {
+        if (lane < T) x = __ldg(indices + a + p);
+        warp_bitonic_sort_keys(x);
+      }
+      if (lane < T) {
+        out[lane] = x;
+        mark(bmb, x);
+      }
+      continue;
+    }
     if (D <= 32) {
       // one chunk: lane p owns position p
       unsigned sel;
@@ -314,8 +366,9 @@ __global__ void __launch_bounds__(256)
                        int G, const int32_t* __restrict__ front, int64_t cap_in, int F,
                        uint64_t level_mix, const uint64_t* __restrict__ rng_seed,
                        int32_t* __restrict__ ell, uint32_t* __restrict__ bm, int64_t nwords,
-                       const int32_t* __restrict__ slow) {
+                       const int32_t* __restrict__ slow, int prng) {
   __shared__ int32_t s_val[2 * kSlowCap];
+  __shared__ uint32_t s_pick[kFloydBits / 32];
   __shared__ uint32_t s_hist[256];
   __shared__ uint64_t s_prefix;
   __shared__ int s_rank, s_fill;
@@ -330,6 +383,32 @@ __global__ void __launch_bounds__(256)
     const int T = min(D, F);
     if (D <= F) {
       for (int p = threadIdx.x; p < D; p += blockDim.x) s_val[p] = indices[a + p];
+    } else if (prng != kSplitMix) {
+      // Floyd over a D-bit membership bitmap (D <= kFloydBits), one thread
+      // draws; then ascending positions are compacted
+      for (int i = threadIdx.x; i < (D + 31) / 32; i += blockDim.x) s_pick[i] = 0u;
+      if (threadIdx.x == 0) s_fill = 0;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const uint64_t sd = mix64(rng_seed[b] ^ level_mix);
+        const uint64_t nk = mix64(((uint64_t)v + 1ull) * GOLDEN ^ sd);
+        Pcg32 g1;
+        Sfc64 g2;
+        Xoshiro256pp g3;
+        g1.seed(nk, sd);
+        g2.seed(nk, sd);
+        g3.seed(nk, sd);
+        for (int j = D - T; j < D; ++j) {
+          const uint32_t n1 = (uint32_t)(j + 1);
+          const int t = (int)(prng == kPcg32 ? g1.bounded(n1)
+                                              : prng == kSfc64 ? g2.bounded(n1) : g3.bounded(n1));
+          const int pick = ((s_pick[t >> 5] >> (t & 31)) & 1u) ? j : t;
+          s_pick[pick >> 5] |= 1u << (pick & 31);
+        }
+      }
+      __syncthreads();
+      for (int p = threadIdx.x; p < D; p += blockDim.x)
+        if ((s_pick[p >> 5] >> (p & 31)) & 1u) s_val[atomicAdd(&s_fill, 1)] = indices[a + p];
     } else {
       // radix-select the T-th smallest key (8 passes of 8 bits), then keep
       // every position whose key is <= it: exactly T positions.
@@ -582,7 +661,8 @@ extern "C" int rg_sample_level(const int64_t* d_indptr, const int32_t* d_indices
                                const int32_t* d_nfront, int32_t fanout, int32_t level,
                                const uint64_t* d_rng_seed, int32_t* d_ell, int32_t* d_cnt,
                                uint32_t* d_bm, int64_t nwords, int32_t* d_slow,
-                               int32_t sorted_rows, void* stream) {
+                               int32_t sorted_rows, int32_t prng, void* stream) {
+  RG_REQUIRE(prng >= kSplitMix && prng <= kXoshiro256pp, "rg_sample_level: unknown prng %d", prng);
   RG_REQUIRE(G >= 1 && cap_in >= 1 && n >= 1, "rg_sample_level: bad sizes");
   RG_REQUIRE(fanout >= 1, "rg_sample_level: fanout must be >= 1");
   if (fanout > kSlowCap) {
@@ -599,11 +679,12 @@ extern "C" int rg_sample_level(const int64_t* d_indptr, const int32_t* d_indices
   sample_level_kernel<<<grid, kSampleWarps * 32, 0, s>>>(d_indptr, d_indices, G, d_front, cap_in,
                                                          d_nfront, fanout, level_mix, d_rng_seed,
                                                          d_ell, d_cnt, d_bm, nwords, slow,
-                                                         sorted_rows);
+                                                         sorted_rows, prng);
   int rc = check_launch("sample_level");
   if (rc || !slow) return rc;
   sample_slow_kernel<<<kNumSMs, 256, 0, s>>>(d_indptr, d_indices, G, d_front, cap_in, fanout,
-                                             level_mix, d_rng_seed, d_ell, d_bm, nwords, slow);
+                                             level_mix, d_rng_seed, d_ell, d_bm, nwords, slow,
+                                             prng);
   return check_launch("sample_slow");
 }
 

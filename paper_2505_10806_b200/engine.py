@@ -75,6 +75,7 @@ class DeviceGraph:
         self.indices = torch.from_numpy(np.ascontiguousarray(indices, dtype=np.int32)).to(self.device)
         self.num_edges = int(self.indices.numel())
         self.sorted_rows = rows_sorted(indptr, indices)
+        self.max_degree = int(np.diff(np.asarray(indptr)).max()) if self.n else 0
 
     @classmethod
     def of(cls, g) -> "DeviceGraph":
@@ -98,11 +99,18 @@ class BlockSampler:
     (ascending src, dst = front[d][b, j]).  front[L] is the input node set.
     """
 
-    def __init__(self, dg: DeviceGraph, fanouts, seed_cap: int, group: int = 1):
+    def __init__(self, dg: DeviceGraph, fanouts, seed_cap: int, group: int = 1,
+                 prng: str = "splitmix"):
         if len(fanouts) == 0:
             raise ValueError("fanouts must be nonempty")
         if any(int(f) < 1 for f in fanouts):
             raise ValueError("fanouts must be >= 1")
+        if prng not in _lib.PRNG_KINDS:
+            raise ValueError(f"unknown prng {prng!r} (one of {sorted(_lib.PRNG_KINDS)})")
+        if prng != "splitmix" and max(int(f) for f in fanouts) > 32 and dg.max_degree > 65536:
+            raise NotImplementedError("PRNG variants with fanout > 32 need degree <= 65536")
+        self.prng = prng
+        self.prng_code = _lib.PRNG_KINDS[prng]
         self.dg = dg
         self.G = int(group)
         self.L = len(fanouts)
@@ -147,7 +155,7 @@ class BlockSampler:
             _lib.call("rg_sample_level", ptr(dg.indptr), ptr(dg.indices), dg.n, G,
                       ptr(self.front[d]), self.caps[d], ptr(self.nfront[d]), self.step_fan[d], d,
                       ptr(self.rng), ptr(self.ell[d]), ptr(self.cnt[d]), ptr(self.bm), dg.nwords,
-                      ptr(self.slow), int(dg.sorted_rows), s)
+                      ptr(self.slow), int(dg.sorted_rows), self.prng_code, s)
             _lib.call("rg_bitmap_compact", ptr(self.bm), dg.nwords, G, ptr(self.chunk),
                       ptr(self.front[d + 1]), self.caps[d + 1], ptr(self.nfront[d + 1]), None, s)
 

@@ -52,16 +52,17 @@ class WorkerPipeline:
     the reference's one-batch-ahead prefetch (prefetch.py:91-164)."""
 
     def __init__(self, dg: DeviceGraph, store: FeatureStore, my_part: int, train_nodes: np.ndarray,
-                 fanouts, batch_size: int, s0: int, group: int, nbuf: int = 2):
+                 fanouts, batch_size: int, s0: int, group: int, nbuf: int = 2,
+                 prng: str = "splitmix"):
         self.dg, self.store, self.my_part = dg, store, int(my_part)
-        self.plan = PlanPass(dg, train_nodes, fanouts, batch_size, s0, group=group)
+        self.plan = PlanPass(dg, train_nodes, fanouts, batch_size, s0, group=group, prng=prng)
         self.sampler: BlockSampler = self.plan.sampler
         self.G = self.plan.G
         self.nb = self.plan.nb
         smp = self.sampler
         self.cap_in = smp.caps[smp.L]
         self.nbuf = int(nbuf)
-        self.samplers = [smp] + [BlockSampler(dg, fanouts, batch_size, group=self.G)
+        self.samplers = [smp] + [BlockSampler(dg, fanouts, batch_size, group=self.G, prng=prng)
                                  for _ in range(self.nbuf - 1)]
         self.row_bufs = [torch.empty((self.G, self.cap_in, store.stride), dtype=torch.float32,
                                      device=dg.device) for _ in range(self.nbuf)]
@@ -183,7 +184,8 @@ class WorkerPipeline:
 
 def run_accounting(g, book, fanouts, batch_size: int, epochs: int, s0: int, mode: str = "rapid",
                    n_hot: int | None = None, n_hot_pct: float = 15.0, hot_scope: str = "epoch",
-                   workers=None, group: int = 16, features: bool = True) -> dict:
+                   workers=None, group: int = 16, features: bool = True,
+                   prng: str = "splitmix") -> dict:
     """Per-worker, per-epoch data-path accounting of the reference's worker
     loop (train.py:171-264 without the SGD step): rpc_calls, nodes_pulled,
     bytes_pulled, cache_hits, cache_misses, reuse_ratio, plus the cache
@@ -211,7 +213,8 @@ def run_accounting(g, book, fanouts, batch_size: int, epochs: int, s0: int, mode
     store.build_route(shard_ids)
     train = np.flatnonzero(g.train_mask)
     workers = list(range(k)) if workers is None else list(workers)
-    pipe0 = WorkerPipeline(dg, store, workers[0], train, fanouts, batch_size, s0, group, nbuf=1)
+    pipe0 = WorkerPipeline(dg, store, workers[0], train, fanouts, batch_size, s0, group, nbuf=1,
+                           prng=prng)
     nb = pipe0.nb
     sched = SeedSchedule(s0, epochs, nb)
     counts = [pipe0.count_epoch(sched, e) for e in range(epochs)]
@@ -222,7 +225,8 @@ def run_accounting(g, book, fanouts, batch_size: int, epochs: int, s0: int, mode
     out = {}
     for p in workers:
         pipe = pipe0 if p == workers[0] else WorkerPipeline(dg, store, p, train, fanouts,
-                                                            batch_size, s0, group, nbuf=1)
+                                                            batch_size, s0, group, nbuf=1,
+                                                            prng=prng)
         pipe.my_part = p
         fill = [0, 0, 0]
         nh = 0

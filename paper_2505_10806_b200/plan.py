@@ -56,6 +56,7 @@ class BatchPlan:
     input_sets: list[list[np.ndarray]] | None
     digest: int = 0
     counts: list[torch.Tensor] = field(default_factory=list, repr=False)
+    prng: str = "splitmix"
     _cache: dict = field(default_factory=dict, repr=False)
 
     @property
@@ -68,7 +69,7 @@ class BatchPlan:
     def block(self, e: int, i: int) -> ComputationBlock:
         """Re-derive the full block, bit-identical to the original (plan.py:57-66)."""
         return sample_block(self.graph, self.batch_seeds[e][i], self.fanouts,
-                            seed_for(self.schedule, e, i), epoch=e, batch=i)
+                            seed_for(self.schedule, e, i), epoch=e, batch=i, prng=self.prng)
 
     def digest_hex(self) -> str:
         return f"{self.digest:016x}"
@@ -87,7 +88,7 @@ class PlanPass:
     permutation, grouped sampling of every batch, access counting."""
 
     def __init__(self, dg: DeviceGraph, train_nodes: np.ndarray, fanouts, batch_size: int,
-                 s0: int, group: int = 16):
+                 s0: int, group: int = 16, prng: str = "splitmix"):
         self.dg = dg
         self.train = torch.from_numpy(np.ascontiguousarray(train_nodes, dtype=np.int32)).to(
             dg.device)
@@ -96,7 +97,8 @@ class PlanPass:
         self.nb = -(-self.n_train // self.batch_size)
         self.s0 = int(s0)
         self.G = max(1, min(int(group), self.nb))
-        self.sampler = BlockSampler(dg, fanouts, self.batch_size, group=self.G)
+        self.prng = prng
+        self.sampler = BlockSampler(dg, fanouts, self.batch_size, group=self.G, prng=prng)
 
     def permutation(self, schedule: SeedSchedule, e: int) -> torch.Tensor:
         return epoch_order_device(self.train, epoch_master(schedule, e))
@@ -125,7 +127,8 @@ class PlanPass:
 
 
 def generate_plan(g, train_nodes: np.ndarray, fanouts: list[int], batch_size: int, epochs: int,
-                  s0: int, keep_inputs: bool = True, group: int = 16) -> BatchPlan:
+                  s0: int, keep_inputs: bool = True, group: int = 16,
+                  prng: str = "splitmix") -> BatchPlan:
     """Precompute every epoch's batches and input sets (plan.py:72-105).
 
     keep_inputs=False skips the host copies of the input sets and the
@@ -138,7 +141,7 @@ def generate_plan(g, train_nodes: np.ndarray, fanouts: list[int], batch_size: in
     batches_per_epoch = -(-len(train_nodes) // batch_size)
     schedule = SeedSchedule(s0=s0, epochs=epochs, batches_per_epoch=batches_per_epoch)
     dg = DeviceGraph.of(g)
-    pp = PlanPass(dg, train_nodes, fanouts, batch_size, s0, group=group)
+    pp = PlanPass(dg, train_nodes, fanouts, batch_size, s0, group=group, prng=prng)
     h = hashlib.blake2b(digest_size=8)
     batch_seeds, input_sets, counts = [], [] if keep_inputs else None, []
     smp = pp.sampler
@@ -166,7 +169,7 @@ def generate_plan(g, train_nodes: np.ndarray, fanouts: list[int], batch_size: in
             input_sets.append(sets_e)
     digest = int.from_bytes(h.digest(), "little") if keep_inputs else 0
     return BatchPlan(graph=g, schedule=schedule, fanouts=list(fanouts), batch_seeds=batch_seeds,
-                     input_sets=input_sets, digest=digest, counts=counts)
+                     input_sets=input_sets, digest=digest, counts=counts, prng=prng)
 
 
 def _owner_u8(book, device) -> torch.Tensor:

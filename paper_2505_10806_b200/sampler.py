@@ -91,20 +91,20 @@ class ComputationBlock:
         return len(self.edges)
 
 
-def _sampler_for(dg: DeviceGraph, fanouts, n_seeds: int) -> BlockSampler:
+def _sampler_for(dg: DeviceGraph, fanouts, n_seeds: int, prng: str = "splitmix") -> BlockSampler:
     """Per-thread cached sampler (its device buffers are per-call scratch,
     so concurrent callers — e.g. the Prefetcher's producer thread and the
     consumer — must not share one)."""
     cap = 1
     while cap < n_seeds:
         cap <<= 1
-    key = (tuple(int(f) for f in fanouts), cap, threading.get_ident())
+    key = (tuple(int(f) for f in fanouts), cap, prng, threading.get_ident())
     cache = dg.__dict__.setdefault("_samplers", {})
     smp = cache.get(key)
     if smp is None:
         if len(cache) > 16:
             cache.clear()
-        smp = BlockSampler(dg, fanouts, cap, group=1)
+        smp = BlockSampler(dg, fanouts, cap, group=1, prng=prng)
         cache[key] = smp
     return smp
 
@@ -130,11 +130,13 @@ def block_from_sampler(smp: BlockSampler, slot: int, seeds: np.ndarray, epoch: i
 
 
 def sample_block(g, seeds: np.ndarray, fanouts: list[int], rng_seed: int, epoch: int = 0,
-                 batch: int = 0) -> ComputationBlock:
+                 batch: int = 0, prng: str = "splitmix") -> ComputationBlock:
     """Build the computation block for one batch of seed nodes (sampler.py:116-152).
 
     fanouts are listed input layer first: expansion step d uses
-    fanouts[len(fanouts)-1-d]."""
+    fanouts[len(fanouts)-1-d].  prng selects the neighbour-selection
+    generator: "splitmix" (the reference's SplitMix64 keys, default) or the
+    variants "pcg32" / "sfc64" / "xoshiro256pp"."""
     if len(fanouts) == 0:
         raise ValueError("fanouts must be nonempty")
     seeds = np.asarray(seeds, dtype=np.int64)
@@ -143,7 +145,7 @@ def sample_block(g, seeds: np.ndarray, fanouts: list[int], rng_seed: int, epoch:
     if seeds.min() < 0 or seeds.max() >= g.num_nodes:
         raise ValueError("seed id out of range")
     dg = DeviceGraph.of(g)
-    smp = _sampler_for(dg, fanouts, len(seeds))
+    smp = _sampler_for(dg, fanouts, len(seeds), prng)
     smp.set_seeds(0, seeds, rng_seed)
     smp.run(1)
     return block_from_sampler(smp, 0, seeds, epoch, batch)

@@ -423,3 +423,45 @@ def test_sage_mean_fwd_bwd_bit_exact(rg):
         dh = sage_mean_backward(dev(dself), dev(dmean), dev(cnt), self_pos,
                                 dev(src_front.astype(np.int32)), dev(ell), F)
         assert np.array_equal(dh.cpu().numpy(), want_dh)
+
+
+@pytest.mark.parametrize("kind", ["pcg32", "sfc64", "xoshiro256pp"])
+def test_prng_variant_blocks_match_oracle(rg, small, kind):
+    """Device PRNG-variant sampling == the variant oracle (fast and CTA paths)."""
+    from oracle import prng_oracle as po
+
+    g2 = rg.synth_powerlaw(20000, 5, 8, 4, seed=7)
+    rng = np.random.default_rng(17)
+    cases = [(small, np.arange(10), [3, 5]), (small, np.arange(40), [40, 48]),
+             (g2, rng.choice(20000, 256, replace=False), [10, 25]),
+             (g2, rng.choice(20000, 64, replace=False), [15, 10, 5])]
+    for g, seeds, fan in cases:
+        s = int(rng.integers(2**63))
+        b = rg.sample_block(g, seeds, fan, s, prng=kind)
+        fr, ed = po.block(g.indptr, g.indices, seeds, fan, s, kind)
+        for a, w in zip(b.frontiers, fr):
+            assert np.array_equal(a, w)
+        for (s1, d1), (s2, d2) in zip(b.edges, ed):
+            assert np.array_equal(s1, s2) and np.array_equal(d1, d2)
+
+
+def test_prng_variant_plan_and_accounting(rg):
+    """The variant flows through the plan pass and the data-path accounting."""
+    from oracle import prng_oracle as po
+    from paper_2505_10806_b200.pipeline import run_accounting
+
+    g = rg.synth_powerlaw(20000, 5, 32, 8, seed=7)
+    book = rg.partition_edgecut(g, 2)
+    train = np.flatnonzero(g.train_mask)
+    plan = rg.generate_plan(g, train, [10, 25], 512, 1, 7, prng="sfc64")
+    sets = []
+    for i, seeds in enumerate(plan.batch_seeds[0]):
+        fr, _ = po.block(g.indptr, g.indices, seeds, [10, 25],
+                         orc.batch_seed(7, 0, i), "sfc64")
+        assert np.array_equal(plan.input_sets[0][i], fr[-1])
+        sets.append(fr[-1])
+    got = run_accounting(g, book, [10, 25], 512, 1, 7, prng="sfc64", workers=[0])
+    all_ids, _ = orc.access_counts(sets, book.owner, 0)
+    hot = orc.hot_set(*orc.access_counts(sets, book.owner, 0), int(len(all_ids) * 15 / 100))
+    fb = sum(orc.route_counts(s, book.owner, 0, hot)[2] for s in sets)
+    assert got[0]["records"][0]["nodes_pulled"] == fb
