@@ -209,6 +209,7 @@ __device__ __forceinline__ int prng_positions(int prng, uint64_t nk, uint64_t sd
   return floyd_positions(g, D, T);
 }
 
+template <bool kVariants>
 __global__ void __launch_bounds__(kSampleWarps * 32)
     sample_level_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                         int G, const int32_t* __restrict__ front, int64_t cap_in,
@@ -264,7 +265,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32)
     }
     int32_t* out = ell + row * F;
     uint32_t* bmb = bm + (int64_t)b * nwords;
-    if (prng != kSplitMix && D > F) {
+    if (kVariants && D > F) {
       const uint64_t sd = seeds_in_smem ? s_seed[b] : mix64(rng_seed[b] ^ level_mix);
       const uint64_t nk = mix64(((uint64_t)v + 1ull) * GOLDEN ^ sd);
       int p = prng_positions(prng, nk, sd, D, T);
@@ -676,10 +677,16 @@ extern "C" int rg_sample_level(const int64_t* d_indptr, const int32_t* d_indices
   if (slow && cudaMemsetAsync(slow, 0, sizeof(int32_t), s) != cudaSuccess)
     return check_launch("sample_level memset");
   const int grid = kNumSMs * 5;  // 48 regs x 256 threads: 5 CTAs per SM
-  sample_level_kernel<<<grid, kSampleWarps * 32, 0, s>>>(d_indptr, d_indices, G, d_front, cap_in,
-                                                         d_nfront, fanout, level_mix, d_rng_seed,
-                                                         d_ell, d_cnt, d_bm, nwords, slow,
-                                                         sorted_rows, prng);
+  // SplitMix64 keys (the reference) and the PRNG variants are separate
+  // instantiations so the reference path keeps its register budget
+  if (prng == kSplitMix)
+    sample_level_kernel<false><<<grid, kSampleWarps * 32, 0, s>>>(
+        d_indptr, d_indices, G, d_front, cap_in, d_nfront, fanout, level_mix, d_rng_seed, d_ell,
+        d_cnt, d_bm, nwords, slow, sorted_rows, prng);
+  else
+    sample_level_kernel<true><<<kNumSMs * 4, kSampleWarps * 32, 0, s>>>(
+        d_indptr, d_indices, G, d_front, cap_in, d_nfront, fanout, level_mix, d_rng_seed, d_ell,
+        d_cnt, d_bm, nwords, slow, sorted_rows, prng);
   int rc = check_launch("sample_level");
   if (rc || !slow) return rc;
   sample_slow_kernel<<<kNumSMs, 256, 0, s>>>(d_indptr, d_indices, G, d_front, cap_in, fanout,
