@@ -40,6 +40,7 @@ CONFIGS = {
     "c1": dict(n=100_000, m=10, d=128, classes=8, fanouts=[10, 5], batch=1024, parts=2),
 }
 S0 = 7
+L2_BYTES = 126 * 2**20
 
 
 def parse():
@@ -91,8 +92,9 @@ class Clocks:
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
         self.source = "nvml"
+        self._nv = self._nvml()  # initialise before the thread starts sampling
 
-    def _run(self):
+    def _nvml(self):
         try:
             import pynvml as nv
 
@@ -102,15 +104,23 @@ class Clocks:
                     nv.nvmlClocksThrottleReasonHwThermalSlowdown,
                     nv.nvmlClocksThrottleReasonSwThermalSlowdown,
                     nv.nvmlClocksThrottleReasonSwPowerCap)
-            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-            while not self._stop.is_set():
-                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-                r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
-                self.samples.append((float(sm), float(mx), [bool(r & b) for b in bits]))
-                self._stop.wait(0.02)
-            return
+            return nv, h, bits, float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
         except Exception:
-            self.source = "nvidia-smi"
+            return None
+
+    def _run(self):
+        if self._nv is not None:
+            nv, h, bits, mx = self._nv
+            while not self._stop.is_set():
+                try:
+                    sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                    r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                    self.samples.append((float(sm), mx, [bool(r & b) for b in bits]))
+                except Exception:
+                    pass
+                self._stop.wait(0.01)
+            return
+        self.source = "nvidia-smi"
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
@@ -344,6 +354,13 @@ def main():
         dist.barrier()
     gev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
+    # inputs smaller than 2x L2 (126 MB): flush L2 between timed steps and time
+    # each step on its own (flush outside the timed spans)
+    feat_bytes = g.num_nodes * d * 4
+    flush = feat_bytes < 2 * L2_BYTES
+    scrub = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device="cuda") if flush else None
+    sev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     timed_batches = []
     launches0 = pipe.launches
@@ -354,14 +371,23 @@ def main():
         start.record()
         pipe.enter_streams()
         for kk in range(args.steps):
+            if flush:
+                pipe.sync_streams()
+                scrub.fill_(float(kk))
+                sev[kk][0].record()
+                pipe.enter_streams()
             i0, ng = step(args.warmup + kk, gev[kk])
             timed_batches.extend(range(i0, i0 + ng))
+            if flush:
+                pipe.sync_streams()
+                sev[kk][1].record()
         pipe.sync_streams()
         end.record()
         torch.cuda.synchronize()
         if args.nvtx:
             torch.cuda.nvtx.range_pop()
-    step_ms_local = start.elapsed_time(end)
+    step_ms_local = (sum(a.elapsed_time(b) for a, b in sev) if flush
+                     else start.elapsed_time(end))
     if args.serial:
         gather_ms = sum(a.elapsed_time(b) for a, b in gev)
     else:
@@ -371,6 +397,8 @@ def main():
             ng = min(G, nb - i0)
             pipe.plan.fill(pipe.perm, 0, i0, ng)
             smp.run(ng)
+            if flush:
+                scrub.fill_(float(kk))
             gev[kk][0].record()
             pipe.gather(ng, i0)
             gev[kk][1].record()
@@ -437,8 +465,11 @@ def main():
                    "partitions": k, "worker": part, "cache_pct": args.cache_pct, "n_hot": n_hot,
                    "prng": args.prng,
                    "batches_per_step": G, "parallelism": f"worker-per-gpu x{world}",
-                   "l2": "inputs larger than L2 (feature shards %.0f MB; bundle %.0f MB/batch)"
-                         % (g.num_nodes * d * 4 / 1e6, float(rows_b.mean()) * d * 4 / 1e6)},
+                   "l2": ("L2 flushed between timed steps (feature table %.0f MB < 2x L2); "
+                          "steps timed individually" if flush else
+                          "inputs larger than L2 (feature shards %.0f MB; bundle %.0f MB/batch)")
+                         % ((feat_bytes / 1e6,) if flush
+                            else (feat_bytes / 1e6, float(rows_b.mean()) * d * 4 / 1e6))},
         "roofline": {"kernel": "gather_bundle_kernel", "bound": "hbm", "achieved": achieved,
                      "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": ncu_traffic("gather_bundle_kernel"),

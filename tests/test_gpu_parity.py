@@ -465,3 +465,58 @@ def test_prng_variant_plan_and_accounting(rg):
     hot = orc.hot_set(*orc.access_counts(sets, book.owner, 0), int(len(all_ids) * 15 / 100))
     fb = sum(orc.route_counts(s, book.owner, 0, hot)[2] for s in sets)
     assert got[0]["records"][0]["nodes_pulled"] == fb
+
+
+def test_products_full_size(rg, golden):
+    """Products shape at full size: inputs hash-equal to the reference's
+    generator, a full epoch of device sampling + gather whose remote-row and
+    RPC accounting equals the survey's oracle figures (SURVEY.md §8a row 14:
+    933,549,256 rows, 11,725 RPCs for worker 0), first and last batch
+    bit-exact against the oracle, bundle rows equal to the feature rows."""
+    import hashlib
+
+    from paper_2505_10806_b200.engine import DeviceGraph, FeatureStore
+    from paper_2505_10806_b200.pipeline import WorkerPipeline
+    from paper_2505_10806_b200.sampler import SeedSchedule, block_from_sampler
+
+    rec = golden["generator"]["products"]
+    n, m, d, c, s = rec["args"]
+    g = rg.synth_powerlaw(n, m, d, c, s)
+    h = lambda a: hashlib.blake2b(np.ascontiguousarray(a).tobytes(),  # noqa: E731
+                                  digest_size=16).hexdigest()
+    assert h(g.indptr.astype("<i8")) == rec["hash"]["indptr"]
+    assert h(g.indices.astype("<i4")) == rec["hash"]["indices"]
+    book = rg.partition_edgecut(g, 8)
+    dg = DeviceGraph(g.indptr, g.indices, g.num_nodes)
+    store = FeatureStore(book.owner, 8, d)
+    ids = [np.flatnonzero(book.owner == q) for q in range(8)]
+    feats = torch.from_numpy(g.features).cuda()
+    for q in range(8):
+        store.set_shard(q, FeatureStore.pad_rows(g.features[ids[q]], store.src_stride, dg.device))
+    store.build_route(ids)
+    train = np.flatnonzero(g.train_mask)
+    pipe = WorkerPipeline(dg, store, 0, train, [15, 10, 5], 1024, 7, 32, nbuf=1)
+    sched = SeedSchedule(7, 1, pipe.nb)
+    pipe.start_epoch(sched, 0)
+    perm = pipe.perm.cpu().numpy()
+    smp = pipe.sampler
+    for i0 in range(0, pipe.nb, pipe.G):
+        ng = pipe.step(i0)
+        if i0 == 0 or i0 + ng == pipe.nb:
+            slot = 0 if i0 == 0 else ng - 1
+            i = i0 + slot
+            seeds = perm[i * 1024:(i + 1) * 1024]
+            blk = block_from_sampler(smp, slot, seeds, 0, i)
+            fr, ed = orc.block(g.indptr, g.indices, seeds, [15, 10, 5], orc.batch_seed(7, 0, i))
+            for a, w in zip(blk.frontiers, fr):
+                assert np.array_equal(a, w), i
+            for (s1, d1), (s2, d2) in zip(blk.edges, ed):
+                assert np.array_equal(s1, s2) and np.array_equal(d1, d2), i
+            nin = len(fr[-1])
+            rows = pipe.rows[slot, :nin, :d]
+            want = feats[torch.from_numpy(fr[-1]).cuda()]
+            assert torch.equal(rows, want), i
+    t = pipe.totals()
+    assert t["bad"] == 0
+    assert t["hit"] + t["fallback"] == 933_549_256
+    assert t["rpcs"] == 11_725
