@@ -173,6 +173,15 @@ int rg_gather_bundle(const int32_t* d_ids, const int32_t* d_nids, int64_t cap, i
                      int32_t stride, int32_t my_part, float* d_out, uint32_t* d_counters,
                      void* stream);
 
+/* Same contract, rows moved by TMA bulk copies (global -> smem -> global),
+ * one warp per CTA, ctas_per_sm CTAs per SM (<= 0: default 4): in-flight
+ * bytes live in shared memory, so the sampler can run concurrently on the
+ * SMs' remaining warp slots and registers.  Rows up to ~1.5 KB.          */
+int rg_gather_bundle_tma(const int32_t* d_ids, const int32_t* d_nids, int64_t cap, int32_t G,
+                         const uint32_t* d_route, const float* const* h_bases,
+                         int32_t src_stride, int32_t stride, int32_t my_part, float* d_out,
+                         uint32_t* d_counters, int32_t ctas_per_sm, void* stream);
+
 /* ---- L5 aggregation consumer (model.py:72-81, 126-135) -------------- */
 /* mean[t] = (sum over t's edges, in stored order, of h[pos(src)]) /
  * max(cnt_t, 1) and self[t] = h[pos(dst_front[t])], positions located by

@@ -25,7 +25,7 @@ struct Bases {
   const float* p[16];
 };
 
-__global__ void __launch_bounds__(kGatherWarps * 32)
+__global__ void __launch_bounds__(kGatherWarps * 32, 4)
     gather_bundle_kernel(const int32_t* __restrict__ ids, const int32_t* __restrict__ nids,
                          int64_t cap, const uint32_t* __restrict__ route, const __grid_constant__ Bases bases,
                          int src_stride, int stride, int nvec, int dq, int dr, int my_part,

@@ -101,11 +101,12 @@ __device__ __forceinline__ unsigned select_mask32(uint64_t key, unsigned cand, i
 
 // Same over up to 64 keys, two per lane (k0: candidate lane, k1: 32+lane).
 __device__ __forceinline__ void select_mask64(uint64_t k0, uint64_t k1, unsigned c0, unsigned c1,
-                                              int need, unsigned& s0, unsigned& s1) {
+                                              int need, unsigned& s0, unsigned& s1,
+                                              int top_bit = 63) {
   s0 = 0;
   s1 = 0;
 #pragma unroll 1
-  for (int bit = 63; bit >= 0; --bit) {
+  for (int bit = top_bit; bit >= 0; --bit) {
     const unsigned o0 = __ballot_sync(kFull, (k0 >> bit) & 1ull);
     const unsigned o1 = __ballot_sync(kFull, (k1 >> bit) & 1ull);
     const unsigned z0 = c0 & ~o0, z1 = c1 & ~o1;
@@ -167,7 +168,8 @@ __device__ __forceinline__ bool select_threshold(uint64_t nk, int D, int T, uint
   const unsigned c0 = __ballot_sync(kFull, lane < count);
   const unsigned c1 = __ballot_sync(kFull, 32 + lane < count);
   unsigned s0, s1;
-  select_mask64(k0, k1, c0, c1, T, s0, s1);
+  // every candidate is < t0: the bits above t0's top bit are zero for all
+  select_mask64(k0, k1, c0, c1, T, s0, s1, 63 - __clzll((long long)t0));
   // compact the selected candidates (already in position order) to lanes
   const int n0 = __popc(s0);
   if ((s0 >> lane) & 1u) s_pos[64 + __popc(s0 & lt)] = s_pos[lane];
@@ -220,36 +222,29 @@ __global__ void __launch_bounds__(kSampleWarps * 32)
   __shared__ int s_next;
   __shared__ uint64_t s_key[kSampleWarps][64];
   __shared__ int32_t s_pos[kSampleWarps][96];
-  __shared__ uint64_t s_seed[kMaxGroupSeeds];  // step seed s_d per batch
-  __shared__ int s_nf[kMaxGroupSeeds];
+  __shared__ uint64_t s_seed[1];  // this CTA's batch step seed s_d
   const int lane = lane_id();
   const int warp = threadIdx.x >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
-  const bool seeds_in_smem = G <= kMaxGroupSeeds;
-  for (int b = threadIdx.x; b < G && seeds_in_smem; b += blockDim.x) {
-    s_seed[b] = mix64(rng_seed[b] ^ level_mix);
-    s_nf[b] = nfront[b];
+  if (threadIdx.x == 0) {
+    s_seed[0] = mix64(rng_seed[blockIdx.y] ^ level_mix);
+    s_next = 0;
   }
-  int maxf = 0;
-  for (int b = lane; b < G; b += 32) maxf = max(maxf, nfront[b]);
-#pragma unroll
-  for (int o = 16; o; o >>= 1) maxf = max(maxf, __shfl_xor_sync(kFull, maxf, o));
-  if (threadIdx.x == 0) s_next = 0;
   __syncthreads();
-  // items k = j*G + b, interleaved so the low (hub-heavy) frontier ranks of
-  // every batch are spread over all CTAs; CTA c owns k = c, c + grid, ...
-  // and its warps pull them dynamically through a shared counter.
-  // (G * max|F| < 2^31: 32-bit index math.)
-  const unsigned total = (unsigned)maxf * (unsigned)G;
-  const unsigned grid = gridDim.x;
+  // batch b = blockIdx.y; its CTAs c = blockIdx.x own frontier ranks
+  // j = c, c + gridDim.x, ... (the low, hub-heavy ranks spread over all of
+  // them) and their warps pull those ranks through a shared counter.
+  const int b = blockIdx.y;
+  const int nfb = nfront[b];
+  const unsigned gx = gridDim.x;
   for (;;) {
     int t = 0;
     if (lane == 0) t = atomicAdd(&s_next, 1);
     t = __shfl_sync(kFull, t, 0);
-    const unsigned k = blockIdx.x + (unsigned)t * grid;
-    if (k >= total) break;
-    const int j = (int)(k / (unsigned)G), b = (int)(k - (unsigned)j * (unsigned)G);
-    if (j >= (seeds_in_smem ? s_nf[b] : nfront[b])) continue;
+    const unsigned ju = blockIdx.x + (unsigned)t * gx;
+    if (ju >= (unsigned)nfb) break;
+    const int j = (int)ju;
+    const unsigned k = (unsigned)j * (unsigned)G + (unsigned)b;  // item id (slow path)
     const int64_t row = (int64_t)b * cap_in + j;
     const int32_t v = front[row];
     const int64_t a = indptr[v];
@@ -266,7 +261,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32)
     int32_t* out = ell + row * F;
     uint32_t* bmb = bm + (int64_t)b * nwords;
     if (kVariants && D > F) {
-      const uint64_t sd = seeds_in_smem ? s_seed[b] : mix64(rng_seed[b] ^ level_mix);
+      const uint64_t sd = s_seed[0];
       const uint64_t nk = mix64(((uint64_t)v + 1ull) * GOLDEN ^ sd);
       int p = prng_positions(prng, nk, sd, D, T);
       int32_t x = INT_MAX;
@@ -290,7 +285,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32)
       if (D <= F) {
         sel = D == 32 ? kFull : ((1u << D) - 1u);
       } else {
-        const uint64_t sd = seeds_in_smem ? s_seed[b] : mix64(rng_seed[b] ^ level_mix);
+        const uint64_t sd = s_seed[0];
         const uint64_t nk = mix64(((uint64_t)v + 1ull) * GOLDEN ^ sd);
         const uint64_t key = lane < D ? mix64(nk + (uint64_t)(lane + 1) * GOLDEN) : ~0ull;
         sel = select_mask32(key, __ballot_sync(kFull, lane < D), T);
@@ -313,7 +308,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32)
       continue;
     }
     // D > 32 (> F): threshold candidates, else the running top-T list
-    const uint64_t sd = seeds_in_smem ? s_seed[b] : mix64(rng_seed[b] ^ level_mix);
+    const uint64_t sd = s_seed[0];
     const uint64_t nk = mix64(((uint64_t)v + 1ull) * GOLDEN ^ sd);
     int pos;
     const bool ordered = select_threshold(nk, D, T, s_key[warp], s_pos[warp], pos);
@@ -664,7 +659,7 @@ extern "C" int rg_sample_level(const int64_t* d_indptr, const int32_t* d_indices
                                uint32_t* d_bm, int64_t nwords, int32_t* d_slow,
                                int32_t sorted_rows, int32_t prng, void* stream) {
   RG_REQUIRE(prng >= kSplitMix && prng <= kXoshiro256pp, "rg_sample_level: unknown prng %d", prng);
-  RG_REQUIRE(G >= 1 && cap_in >= 1 && n >= 1, "rg_sample_level: bad sizes");
+  RG_REQUIRE(G >= 1 && G <= 65535 && cap_in >= 1 && n >= 1, "rg_sample_level: bad sizes");
   RG_REQUIRE(fanout >= 1, "rg_sample_level: fanout must be >= 1");
   if (fanout > kSlowCap) {
     set_error("rg_sample_level: fanout %d above the supported %d", fanout, kSlowCap);
@@ -680,11 +675,13 @@ extern "C" int rg_sample_level(const int64_t* d_indptr, const int32_t* d_indices
   // SplitMix64 keys (the reference) and the PRNG variants are separate
   // instantiations so the reference path keeps its register budget
   if (prng == kSplitMix)
-    sample_level_kernel<false><<<grid, kSampleWarps * 32, 0, s>>>(
-        d_indptr, d_indices, G, d_front, cap_in, d_nfront, fanout, level_mix, d_rng_seed, d_ell,
-        d_cnt, d_bm, nwords, slow, sorted_rows, prng);
+    sample_level_kernel<false><<<dim3(std::max(1, grid / G), G), kSampleWarps * 32, 0,
+                                 s>>>(d_indptr, d_indices, G, d_front, cap_in, d_nfront, fanout,
+                                      level_mix, d_rng_seed, d_ell, d_cnt, d_bm, nwords, slow,
+                                      sorted_rows, prng);
   else
-    sample_level_kernel<true><<<kNumSMs * 4, kSampleWarps * 32, 0, s>>>(
+    sample_level_kernel<true><<<dim3(std::max(1, kNumSMs * 4 / G), G),
+                                kSampleWarps * 32, 0, s>>>(
         d_indptr, d_indices, G, d_front, cap_in, d_nfront, fanout, level_mix, d_rng_seed, d_ell,
         d_cnt, d_bm, nwords, slow, sorted_rows, prng);
   int rc = check_launch("sample_level");
