@@ -428,6 +428,7 @@ def main():
     per_batch = tot["per_batch"]
     rows_b = per_batch[:, 0] + per_batch[:, 1] + per_batch[:, 2]
     timed_rows = int(sum(rows_b[i] for i in timed_batches))
+    peer_rows = int(sum(per_batch[i, 5] for i in timed_batches))
 
     # roofline of the dominant kernel (bundle gather): read + write every row,
     # plus the id and route word per row
@@ -477,6 +478,13 @@ def main():
                      "share_of_step": gather_ms / step_ms_local,
                      "step_frac": step_bytes / (step_ms_local / 1e3) / 1e9 / peak},
         "e2e": e2e,
+        "nvlink": ({"peer_rows_per_batch": peer_rows / max(1, n_batches),
+                    "bytes_per_batch": peer_rows * 4 * d / max(1, n_batches),
+                    "achieved_gbs": peer_rows * 4 * d / (gather_ms / 1e3) / 1e9,
+                    "peer_copy_ref_gbs": 770.0,
+                    "note": "peer-shard payload bytes read by the gather over NVLink, timed "
+                            "with the gather alone; 770 GB/s = measured peer copy per "
+                            "direction (B200_PROFILING.md)"} if world > 1 else None),
         "gpu_launches": gpu_launches,
         "clocks": clk.summary(),
         "remote_rows_epoch": {"worker": part, "uncached": remote_rows,

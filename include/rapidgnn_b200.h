@@ -52,6 +52,7 @@ extern "C" {
 #define RG_CNT_FALLBACK 2
 #define RG_CNT_OWNER_MASK 3 /* bit q set <=> >=1 fallback row owned by q */
 #define RG_CNT_BAD 4        /* rows whose route was RG_ROUTE_INVALID     */
+#define RG_CNT_PEER 5       /* fallback rows read from a peer GPU's shard */
 #define RG_NCOUNTERS 8
 
 const char* rg_last_error(void);
@@ -164,14 +165,15 @@ int rg_route_with_cache(const uint32_t* d_base_route, int64_t n, const int32_t* 
  * (partition shard or cache).  Classification per row: kind == my_part ->
  * local, kind == RG_KIND_CACHE -> cache hit, else fallback pull from shard
  * `kind`.  d_counters: G x RG_NCOUNTERS uint32, accumulated (caller zeroes).
- * h_bases: host array of 16 device pointers (peer pointers allowed).
+ * h_bases: host array of 16 device pointers (peer pointers allowed);
+ * peer_mask: bit q set if shard q lives on another GPU (RG_CNT_PEER).
  * stride, src_stride: floats, multiples of 4 (16-byte rows); src_stride >=
  * stride lets sources keep sector/line-aligned padded rows (NVLink reads
  * run at full rate on 128-byte-aligned rows) while the bundle stays dense. */
 int rg_gather_bundle(const int32_t* d_ids, const int32_t* d_nids, int64_t cap, int32_t G,
                      const uint32_t* d_route, const float* const* h_bases, int32_t src_stride,
-                     int32_t stride, int32_t my_part, float* d_out, uint32_t* d_counters,
-                     void* stream);
+                     int32_t stride, int32_t my_part, uint32_t peer_mask, float* d_out,
+                     uint32_t* d_counters, void* stream);
 
 /* Same contract, rows moved by TMA bulk copies (global -> smem -> global),
  * one warp per CTA, ctas_per_sm CTAs per SM (<= 0: default 4): in-flight

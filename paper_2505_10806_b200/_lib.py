@@ -27,6 +27,7 @@ RG_ROW_MASK = 0x0FFFFFFF
 RG_ROUTE_INVALID = 0xFFFFFFFF
 RG_MAX_PARTS = 15
 RG_CNT_LOCAL, RG_CNT_HIT, RG_CNT_FALLBACK, RG_CNT_OWNER_MASK, RG_CNT_BAD = 0, 1, 2, 3, 4
+RG_CNT_PEER = 5
 RG_NCOUNTERS = 8
 PRNG_KINDS = {"splitmix": 0, "pcg32": 1, "sfc64": 2, "xoshiro256pp": 3}
 
@@ -54,8 +55,8 @@ _SIGNATURES = {
     "rg_threshold_split": (c_int32, [P, P, c_int64, c_uint32, P, P, P]),
     "rg_gather_counts": (c_int32, [P, P, P, c_int64, P, P]),
     "rg_route_with_cache": (c_int32, [P, c_int64, P, c_int64, P, P]),
-    "rg_gather_bundle": (c_int32, [P, P, c_int64, c_int32, P, P, c_int32, c_int32, c_int32, P, P,
-                                   P]),
+    "rg_gather_bundle": (c_int32, [P, P, c_int64, c_int32, P, P, c_int32, c_int32, c_int32,
+                                   c_uint32, P, P, P]),
     "rg_gather_bundle_tma": (c_int32, [P, P, c_int64, c_int32, P, P, c_int32, c_int32, c_int32,
                                        P, P, c_int32, P]),
     "rg_sage_mean_fwd": (c_int32, [P, c_int64, c_int32, c_int32, P, P, c_int64, P, P, c_int32, P,

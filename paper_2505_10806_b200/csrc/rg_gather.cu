@@ -29,7 +29,8 @@ __global__ void __launch_bounds__(kGatherWarps * 32, 4)
     gather_bundle_kernel(const int32_t* __restrict__ ids, const int32_t* __restrict__ nids,
                          int64_t cap, const uint32_t* __restrict__ route, const __grid_constant__ Bases bases,
                          int src_stride, int stride, int nvec, int dq, int dr, int my_part,
-                         float* __restrict__ out, uint32_t* __restrict__ counters) {
+                         uint32_t peer_mask, float* __restrict__ out,
+                         uint32_t* __restrict__ counters) {
   __shared__ uint32_t s_cnt[RG_NCOUNTERS];
   __shared__ const float* s_base[16];
   const int b = blockIdx.y;
@@ -39,7 +40,7 @@ __global__ void __launch_bounds__(kGatherWarps * 32, 4)
   if (threadIdx.x < 16) s_base[threadIdx.x] = bases.p[threadIdx.x];
   __syncthreads();
   const int nrows = nids[b];
-  uint32_t c_local = 0, c_hit = 0, c_fb = 0, c_bad = 0, omask = 0;
+  uint32_t c_local = 0, c_hit = 0, c_fb = 0, c_bad = 0, c_peer = 0, omask = 0;
   const int64_t warp_stride = (int64_t)gridDim.x * kGatherWarps * 32;
   for (int64_t r0 = ((int64_t)blockIdx.x * kGatherWarps + warp) * 32; r0 < nrows;
        r0 += warp_stride) {
@@ -58,6 +59,7 @@ __global__ void __launch_bounds__(kGatherWarps * 32, 4)
     c_hit += __popc(__ballot_sync(kFull, hit));
     c_fb += __popc(__ballot_sync(kFull, fb));
     c_bad += __popc(__ballot_sync(kFull, bad));
+    c_peer += __popc(__ballot_sync(kFull, fb && ((peer_mask >> kind) & 1u)));
     omask |= __reduce_or_sync(kFull, fb ? (1u << kind) : 0u);
     const float* src = nullptr;
     if (bp) src = bp + (int64_t)(rt & RG_ROW_MASK) * src_stride;
@@ -101,6 +103,7 @@ __global__ void __launch_bounds__(kGatherWarps * 32, 4)
     atomicAdd(&s_cnt[RG_CNT_HIT], c_hit);
     atomicAdd(&s_cnt[RG_CNT_FALLBACK], c_fb);
     atomicAdd(&s_cnt[RG_CNT_BAD], c_bad);
+    atomicAdd(&s_cnt[RG_CNT_PEER], c_peer);
     atomicOr(&s_cnt[RG_CNT_OWNER_MASK], omask);
   }
   __syncthreads();
@@ -143,8 +146,9 @@ using namespace rg;
 
 extern "C" int rg_gather_bundle(const int32_t* d_ids, const int32_t* d_nids, int64_t cap,
                                 int32_t G, const uint32_t* d_route, const float* const* h_bases,
-                                int32_t src_stride, int32_t stride, int32_t my_part, float* d_out,
-                                uint32_t* d_counters, void* stream) {
+                                int32_t src_stride, int32_t stride, int32_t my_part,
+                                uint32_t peer_mask, float* d_out, uint32_t* d_counters,
+                                void* stream) {
   RG_REQUIRE(G >= 1 && G <= 65535 && cap >= 1, "rg_gather_bundle: bad sizes");
   RG_REQUIRE(stride >= 4 && stride % 4 == 0, "rg_gather_bundle: stride %d not a multiple of 4",
              stride);
@@ -170,8 +174,8 @@ extern "C" int rg_gather_bundle(const int32_t* d_ids, const int32_t* d_nids, int
   const int gx = (int)std::max<int64_t>(
       1, std::min<int64_t>(want, ((int64_t)kNumSMs * ctas_per_sm + G - 1) / G));
   gather_bundle_kernel<<<dim3(gx, G), kGatherWarps * 32, 0, (cudaStream_t)stream>>>(
-      d_ids, d_nids, cap, d_route, bases, src_stride, stride, nvec, dq, dr, my_part, d_out,
-      d_counters);
+      d_ids, d_nids, cap, d_route, bases, src_stride, stride, nvec, dq, dr, my_part, peer_mask,
+      d_out, d_counters);
   return check_launch("gather_bundle");
 }
 

@@ -229,10 +229,15 @@ class FeatureStore:
         self.shards: list[torch.Tensor | None] = [None] * self.k
         self.bases = [0] * 16
         self.route = None
+        self.peer_mask = 0  # bit q: shard q is another GPU's memory (NVLink)
 
     def set_shard(self, q: int, rows: torch.Tensor | None, base: int | None = None) -> None:
         self.shards[q] = rows
         self.bases[q] = int(base if base is not None else (rows.data_ptr() if rows is not None else 0))
+        if rows is None and base:
+            self.peer_mask |= 1 << q
+        else:
+            self.peer_mask &= ~(1 << q)
 
     def build_route(self, shard_ids: list[np.ndarray | None]) -> None:
         self.route = as_i32_bits(route_table(self.owner_np, shard_ids)).to(self.device)
@@ -254,10 +259,10 @@ def bases_array(bases) -> np.ndarray:
 
 def gather_bundle(ids: torch.Tensor, nids: torch.Tensor, cap: int, G: int, route: torch.Tensor,
                   bases: np.ndarray, src_stride: int, stride: int, my_part: int,
-                  out: torch.Tensor, counters: torch.Tensor) -> None:
+                  out: torch.Tensor, counters: torch.Tensor, peer_mask: int = 0) -> None:
     """rg_gather_bundle on the current stream (bases: host uint64[16])."""
     _lib.call("rg_gather_bundle", ptr(ids), ptr(nids), cap, G, ptr(route), bases.ctypes.data,
-              src_stride, stride, my_part, ptr(out), ptr(counters), _cur())
+              src_stride, stride, my_part, peer_mask, ptr(out), ptr(counters), _cur())
 
 
 def gather_rows(base: torch.Tensor, row_idx: np.ndarray | torch.Tensor, stride: int,

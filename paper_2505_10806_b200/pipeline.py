@@ -102,7 +102,7 @@ class WorkerPipeline:
             nids = torch.tensor([n_hot], dtype=I32, device=self.dg.device)
             _lib.call("rg_gather_bundle", ptr(hot_ids), ptr(nids), n_hot, 1, ptr(st.route),
                       bases_array(st.bases).ctypes.data, st.src_stride, st.src_stride, -1,
-                      ptr(rows), ptr(cnt), s)
+                      st.peer_mask, ptr(rows), ptr(cnt), s)
         _lib.call("rg_route_with_cache", ptr(st.route), st.n, ptr(hot_ids), n_hot, ptr(route), s)
         c = cnt.cpu().numpy()[0].view(np.uint32)
         rpcs = bin(int(c[_lib.RG_CNT_OWNER_MASK])).count("1")
@@ -167,7 +167,7 @@ class WorkerPipeline:
             route = self.cache.route
         _lib.call("rg_gather_bundle", ptr(smp.front[smp.L]), ptr(smp.nfront[smp.L]), self.cap_in,
                   ng, ptr(route), bases_array(bases).ctypes.data, st.src_stride, st.stride,
-                  self.my_part,
+                  self.my_part, st.peer_mask,
                   ptr(rows), ptr(self.counters) + i0 * _lib.RG_NCOUNTERS * 4,
                   _lib.stream_handle())
 
@@ -179,7 +179,7 @@ class WorkerPipeline:
         rpcs = int(sum(bin(int(m)).count("1") for m in masks))
         return {"local": int(c[:, 0].sum()), "hit": int(c[:, 1].sum()),
                 "fallback": int(c[:, 2].sum()), "bad": int(c[:, 4].sum()), "rpcs": rpcs,
-                "per_batch": c}
+                "peer": int(c[:, _lib.RG_CNT_PEER].sum()), "per_batch": c}
 
 
 def run_accounting(g, book, fanouts, batch_size: int, epochs: int, s0: int, mode: str = "rapid",

@@ -27,7 +27,7 @@ def run(kind, per_sm=0):
     s = _lib.stream_handle()
     if kind == "ldg":
         _lib.call("rg_gather_bundle", ptr(ids), ptr(nids), nrow, G, ptr(route), bases.ctypes.data,
-                  d, d, -1, ptr(out), ptr(cnt), s)
+                  d, d, -1, 0, ptr(out), ptr(cnt), s)
     else:
         _lib.call("rg_gather_bundle_tma", ptr(ids), ptr(nids), nrow, G, ptr(route),
                   bases.ctypes.data, d, d, -1, ptr(out), ptr(cnt), per_sm, s)
