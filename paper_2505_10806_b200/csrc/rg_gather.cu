@@ -166,13 +166,17 @@ extern "C" int rg_gather_bundle(const int32_t* d_ids, const int32_t* d_nids, int
 
   // enough CTAs for ~4 resident per SM on the largest slot; extra CTAs of a
   // short batch exit after one bounds check.
+  // One wave: (SMs x 3) CTAs split evenly over the G batches (each CTA
+  // grid-strides over its batch's rows).  Measured (profiles/r01_summary.md):
+  // 3/SM single wave 6.39 TB/s; 4/SM (a 16-CTA second wave at G=32) 5.15;
+  // 8/SM (two waves) 5.94.
   static const int ctas_per_sm = [] {
     const char* e = getenv("RG_GATHER_CTAS_PER_SM");
-    return e ? std::max(1, atoi(e)) : 8;
+    return e ? std::max(1, atoi(e)) : 3;
   }();
   const int64_t want = (cap + kGatherWarps * 32 - 1) / (kGatherWarps * 32);
   const int gx = (int)std::max<int64_t>(
-      1, std::min<int64_t>(want, ((int64_t)kNumSMs * ctas_per_sm + G - 1) / G));
+      1, std::min<int64_t>(want, ((int64_t)kNumSMs * ctas_per_sm) / G));
   gather_bundle_kernel<<<dim3(gx, G), kGatherWarps * 32, 0, (cudaStream_t)stream>>>(
       d_ids, d_nids, cap, d_route, bases, src_stride, stride, nvec, dq, dr, my_part, peer_mask,
       d_out, d_counters);
