@@ -520,3 +520,43 @@ def test_products_full_size(rg, golden):
     assert t["bad"] == 0
     assert t["hit"] + t["fallback"] == 933_549_256
     assert t["rpcs"] == 11_725
+
+
+@pytest.mark.parametrize("mode", ["rapid", "baseline"])
+def test_training_run_matches_reference_records(rg, golden, mode, tmp_path):
+    """train.run on the device (data path + GraphSAGE step + SGD + eval)
+    against the reference's REPLAY run: accounting columns and digest
+    bit-exact, loss within rel 1e-5, train accuracy within 1e-3."""
+    from paper_2505_10806_b200.train import RunConfig, read_metrics, run, worker_metrics_path
+
+    cfg = RunConfig(**golden["replay"]["config"], mode=mode,
+                    metrics_out=str(tmp_path / "m.csv"))
+    res = run(cfg)
+    ref = golden["replay"][mode]
+    for r, w in zip(res, ref):
+        assert r.plan_digest == w["digest"] == "31a0e51d3b2d9a8c"
+        assert list(r.cache_fill) == w["fill"]
+        for rec, we in zip(r.records, w["epochs"]):
+            assert [rec.rpc_calls, rec.nodes_pulled, rec.bytes_pulled, rec.cache_hits,
+                    rec.cache_misses, rec.reuse_ratio] == we[:6]
+            assert rec.loss == pytest.approx(we[6], rel=1e-5)
+            assert abs(rec.train_acc - we[7]) <= 1e-3
+        csv_rec = read_metrics(worker_metrics_path(cfg.metrics_out, r.part))
+        assert [c.nodes_pulled for c in csv_rec] == [x.nodes_pulled for x in r.records]
+
+
+def test_training_mode_equivalence(rg, golden):
+    """Criterion 3 of the reference acceptance suite (test_acceptance.py:113-122):
+    rapid and baseline consume bit-identical rows, so losses, accuracies and
+    final parameters are identical."""
+    from paper_2505_10806_b200.train import RunConfig, run
+
+    base = dict(golden["replay"]["config"], epochs=2)
+    a = run(RunConfig(**base, mode="rapid"))
+    b = run(RunConfig(**base, mode="baseline"))
+    for ra, rb in zip(a, b):
+        assert [x.loss for x in ra.records] == [x.loss for x in rb.records]
+        assert [x.train_acc for x in ra.records] == [x.train_acc for x in rb.records]
+        for pa, pb in zip(ra.params, rb.params):
+            assert torch.equal(pa.w_self, pb.w_self) and torch.equal(pa.w_neigh, pb.w_neigh)
+            assert torch.equal(pa.bias, pb.bias)
