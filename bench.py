@@ -278,6 +278,7 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "WARN")  # stdout carries only the JSON line
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     from paper_2505_10806_b200 import _lib
