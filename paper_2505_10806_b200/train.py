@@ -23,8 +23,9 @@ import torch
 
 from . import model
 from .engine import DeviceGraph, FeatureStore
-from .graph import synth_powerlaw
-from .partition import halo_expand, partition_edgecut, partition_random
+from .graph import load_graph, synth_powerlaw
+from .partition import (halo_expand, load_partition, partition_edgecut,
+                        partition_random)
 from .pipeline import WorkerPipeline, resolve_n_hot
 from .plan import candidates, generate_plan
 from .rng import mix64
@@ -135,14 +136,16 @@ class WorkerResult:
 
 
 def _graph_and_book(cfg: RunConfig):
-    if cfg.graph_path:
-        raise NotImplementedError("RGF1 loading is outside the device data path")
-    g = synth_powerlaw(cfg.gen_nodes, cfg.gen_edges_per_node, cfg.feat_dim, cfg.num_classes,
-                       cfg.s0)
+    """train.py:148-162: RGF1 file or generator; RPB1 file or partitioner."""
+    g = (load_graph(cfg.graph_path) if cfg.graph_path else
+         synth_powerlaw(cfg.gen_nodes, cfg.gen_edges_per_node, cfg.feat_dim, cfg.num_classes,
+                        cfg.s0))
     if cfg.partition_path:
-        raise NotImplementedError("RPB1 loading is outside the device data path")
-    book = (partition_random(g, cfg.partitions, cfg.s0) if cfg.partitioner == "random"
-            else partition_edgecut(g, cfg.partitions))
+        book = load_partition(cfg.partition_path)
+    elif cfg.partitioner == "random":
+        book = partition_random(g, cfg.partitions, cfg.s0)
+    else:
+        book = partition_edgecut(g, cfg.partitions)
     return g, halo_expand(g, book)
 
 
