@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--nvtx", action="store_true", help="NVTX range 'timed' around the timed steps")
     ap.add_argument("--serial", action="store_true",
                     help="no sample/gather overlap (one stream, per-kernel timing)")
+    ap.add_argument("--graphs", action="store_true",
+                    help="replay each group's launches from a captured CUDA graph (serial)")
     return ap.parse_args()
 
 
@@ -306,7 +308,7 @@ def main():
     store.build_route(shard_ids)
     train = np.flatnonzero(g.train_mask)
     pipe = WorkerPipeline(dg, store, part, train, cfg["fanouts"], cfg["batch"], S0, args.group,
-                          nbuf=1 if args.serial else 2, prng=args.prng)
+                          nbuf=1 if (args.serial or args.graphs) else 2, prng=args.prng)
     nb, G = pipe.nb, pipe.G
     sched = SeedSchedule(S0, 1, nb)
 
@@ -333,6 +335,8 @@ def main():
 
     def step(kk, timed_events=None):
         i0 = (kk % n_full) * G
+        if args.graphs:
+            return i0, pipe.step_graph(i0)
         if not args.serial:
             return i0, pipe.step_overlapped(i0)
         ng = min(G, nb - i0)
@@ -349,6 +353,9 @@ def main():
     pipe.enter_streams()
     for kk in range(args.warmup):
         step(kk)
+    if args.graphs:  # capture every group's graph before timing
+        for kk in range(min(n_full, args.warmup + args.steps)):
+            pipe.step_graph(kk * G)
     pipe.sync_streams()
     torch.cuda.synchronize()
     if world > 1:
@@ -389,7 +396,7 @@ def main():
             torch.cuda.nvtx.range_pop()
     step_ms_local = (sum(a.elapsed_time(b) for a, b in sev) if flush
                      else start.elapsed_time(end))
-    if args.serial:
+    if args.serial and not args.graphs:
         gather_ms = sum(a.elapsed_time(b) for a, b in gev)
     else:
         # overlapped run: time the gather alone on the same batches (serial)

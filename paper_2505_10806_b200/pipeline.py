@@ -125,6 +125,30 @@ class WorkerPipeline:
         self.launches += 1 + 1 + 2 + smp.L * 3 + 1
         return ng
 
+    def step_graph(self, i0: int) -> int:
+        """step(i0) replayed from a CUDA graph captured on first use (one
+        graph per group start: i0 is a kernel argument).  Removes the
+        per-launch host cost, which dominates small graphs (C1: ~41 MB per
+        batch, 6 us at HBM speed)."""
+        ng = min(self.G, self.nb - i0)
+        key = (self.epoch, i0, ng)
+        graphs = self.__dict__.setdefault("_graphs", {})
+        gr = graphs.get(key)
+        if gr is None:
+            if len(graphs) > 4096:
+                graphs.clear()
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):  # warm the allocator outside capture
+                self.step(i0)
+            torch.cuda.current_stream().wait_stream(side)
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr):
+                self.step(i0)
+            graphs[key] = gr
+        gr.replay()
+        return ng
+
     def step_overlapped(self, i0: int) -> int:
         """Like step(), but sampling and gather of consecutive groups overlap
         on two streams (buffer k % nbuf).  Call sync_streams() before reading
