@@ -38,6 +38,10 @@ CONFIGS = {
                      parts=8),
     "reddit": dict(n=232_965, m=246, d=602, classes=41, fanouts=[25, 10], batch=1024, parts=8),
     "c1": dict(n=100_000, m=10, d=128, classes=8, fanouts=[10, 5], batch=1024, parts=2),
+    # config X: structure / masks / partition from the bit-exact native
+    # generator; feature rows generated on the device (rg_fill_features)
+    "papers100m": dict(n=111_059_956, m=7, d=128, classes=172, fanouts=[15, 10, 5], batch=4096,
+                       parts=8, device_features=True, group=4),
 }
 S0 = 7
 L2_BYTES = 126 * 2**20
@@ -50,7 +54,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="products", choices=sorted(CONFIGS))
-    ap.add_argument("--group", type=int, default=32)
+    ap.add_argument("--group", type=int, default=0, help="batches per step (0: config default)")
+    ap.add_argument("--check", action="store_true",
+                    help="verify one batch bit-exactly against the CPU oracle after timing")
     ap.add_argument("--cache-pct", type=float, default=15.0)
     ap.add_argument("--prng", default="splitmix",
                     choices=["splitmix", "pcg32", "sfc64", "xoshiro256pp"])
@@ -75,7 +81,9 @@ def build_inputs(cfg):
     from paper_2505_10806_b200.partition import partition_edgecut
 
     t = time.time()
-    g = synth_powerlaw(cfg["n"], cfg["m"], cfg["d"], cfg["classes"], S0)
+    big = cfg.get("device_features", False)
+    g = synth_powerlaw(cfg["n"], cfg["m"], cfg["d"], cfg["classes"], S0, with_features=not big,
+                       with_labels=not big)
     book = partition_edgecut(g, cfg["parts"])
     log(f"[bench] inputs: n={g.num_nodes} E={g.num_edges} in {time.time() - t:.1f}s")
     return g, book
@@ -300,14 +308,23 @@ def main():
     store = FeatureStore(owner, k, d)
     shard_ids = [np.flatnonzero(owner == q) for q in range(k)]
     for q in range(k):
-        if q % world == rank:
+        if q % world != rank:
+            continue
+        if cfg.get("device_features"):
+            ids_q = torch.from_numpy(shard_ids[q].astype(np.int32)).cuda()
+            rows = torch.empty((len(shard_ids[q]), store.src_stride), device="cuda")
+            _lib.call("rg_fill_features", ids_q.data_ptr(), len(shard_ids[q]), d,
+                      store.src_stride, S0, rows.data_ptr(), _lib.stream_handle())
+            store.set_shard(q, rows)
+        else:
             store.set_shard(q, FeatureStore.pad_rows(g.features[shard_ids[q]], store.src_stride,
                                                      dg.device))
     if world > 1:
         multigpu.exchange_shards(store, rank, world)
     store.build_route(shard_ids)
     train = np.flatnonzero(g.train_mask)
-    pipe = WorkerPipeline(dg, store, part, train, cfg["fanouts"], cfg["batch"], S0, args.group,
+    group = args.group or cfg.get("group", 32)
+    pipe = WorkerPipeline(dg, store, part, train, cfg["fanouts"], cfg["batch"], S0, group,
                           nbuf=1 if (args.serial or args.graphs) else 2, prng=args.prng)
     nb, G = pipe.nb, pipe.G
     sched = SeedSchedule(S0, 1, nb)
@@ -451,7 +468,8 @@ def main():
         e2e = run_e2e(pipe, g, cfg, args, world)
 
     result = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    check = run_check(pipe, g, cfg, S0) if (args.check and rank == 0) else None
+    if rank == 0 and world == 1 and not args.no_cpu and not cfg.get("device_features"):
         hot_np = hot.cpu().numpy().astype(np.int64)
         result = cpu_baseline(cpu_state(g, book, cfg, hot_np, part), args.cpu_seconds, nb)
 
@@ -500,10 +518,44 @@ def main():
                               "rpcs": tot["rpcs"], "reduction": remote_rows / max(1, tot["fallback"]),
                               "bad": tot["bad"], "epoch_ms": epoch_ms, "plan_pass_ms": plan_ms},
         "cpu_baseline": result,
+        "check": check,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_check(pipe, g, cfg, s0):
+    """Batch 0 of the epoch against the CPU oracle: frontiers and edges
+    bit-exact; bundle rows bit-exact against the feature rows of its input
+    nodes (re-generated / read independently of the gather)."""
+    import torch
+
+    from oracle import gnn_oracle as orc
+    from paper_2505_10806_b200 import _lib
+    from paper_2505_10806_b200.sampler import block_from_sampler
+
+    smp = pipe.sampler
+    pipe.step(0)
+    perm = pipe.perm[: cfg["batch"]].cpu().numpy()
+    blk = block_from_sampler(smp, 0, perm, 0, 0)
+    t = time.time()
+    fr, ed = orc.block(g.indptr, g.indices, perm, cfg["fanouts"], orc.batch_seed(s0, 0, 0))
+    ok = all(np.array_equal(a, b) for a, b in zip(blk.frontiers, fr))
+    ok = ok and all(np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+                    for a, b in zip(blk.edges, ed))
+    ids = torch.from_numpy(fr[-1].astype(np.int32)).cuda()
+    d = cfg["d"]
+    if cfg.get("device_features"):
+        want = torch.empty((len(ids), pipe.store.src_stride), device="cuda")
+        _lib.call("rg_fill_features", ids.data_ptr(), len(ids), d, pipe.store.src_stride, s0,
+                  want.data_ptr(), _lib.stream_handle())
+        want = want[:, :d]
+    else:
+        want = torch.from_numpy(g.features[fr[-1]]).cuda()
+    rows_ok = bool(torch.equal(pipe.rows[0, : len(ids), :d], want))
+    return {"batch": 0, "input_nodes": int(len(fr[-1])), "blocks_bit_exact": bool(ok),
+            "rows_bit_exact": rows_ok, "oracle_s": round(time.time() - t, 1)}
 
 
 def run_e2e(pipe, g, cfg, args, world):

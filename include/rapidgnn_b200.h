@@ -148,6 +148,11 @@ int rg_count_histogram(const uint32_t* d_counts, const uint8_t* d_owner, int32_t
  * count > c_star, bm_eq = candidates with count == c_star.             */
 int rg_threshold_split(const uint32_t* d_counts, const uint32_t* d_bm_cand, int64_t n,
                        uint32_t c_star, uint32_t* d_bm_gt, uint32_t* d_bm_eq, void* stream);
+/* synthetic feature rows for config X (the reference's numpy generator
+ * does not scale to 1e8 nodes): row of node ids[i] -> out[i*stride],
+ * value(v,c) = Box-Muller normal from mix64(seed ^ ((v*d+c+1)*GOLDEN)).  */
+int rg_fill_features(const int32_t* d_ids, int64_t n, int32_t d, int32_t stride, uint64_t seed,
+                     float* d_out, void* stream);
 /* out[i] = counts[ids[i]] (FrequencyTable.counts)                      */
 int rg_gather_counts(const uint32_t* d_counts, const int32_t* d_ids, const int32_t* d_n,
                      int64_t cap, uint32_t* d_out, void* stream);

@@ -54,6 +54,7 @@ _SIGNATURES = {
     "rg_count_histogram": (c_int32, [P, P, c_int32, c_int64, P, c_int32, P, P]),
     "rg_threshold_split": (c_int32, [P, P, c_int64, c_uint32, P, P, P]),
     "rg_gather_counts": (c_int32, [P, P, P, c_int64, P, P]),
+    "rg_fill_features": (c_int32, [P, c_int64, c_int32, c_int32, c_uint64, P, P]),
     "rg_route_with_cache": (c_int32, [P, c_int64, P, c_int64, P, P]),
     "rg_gather_bundle": (c_int32, [P, P, c_int64, c_int32, P, P, c_int32, c_int32, c_int32,
                                    c_uint32, P, P, P]),

@@ -123,6 +123,29 @@ __global__ void fill_seeds_kernel(const int32_t* __restrict__ perm, int64_t n_pe
   }
 }
 
+// Synthetic feature rows for graphs too large for the reference's numpy
+// generator (config X): value(v, c) = Box-Muller normal of two 24-bit
+// uniforms from mix64(seed ^ ((v * d + c + 1) * GOLDEN)).  Row of node ids[i]
+// goes to out[i * stride]; padding columns are zero.
+__global__ void fill_features_kernel(const int32_t* __restrict__ ids, int64_t n, int d,
+                                     int stride, uint64_t seed, float* __restrict__ out) {
+  const int64_t total = n * stride;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / stride;
+    const int c = (int)(e - i * stride);
+    float val = 0.f;
+    if (c < d) {
+      const uint64_t v = (uint64_t)ids[i];
+      const uint64_t h = mix64(seed ^ ((v * (uint64_t)d + (uint64_t)c + 1ull) * GOLDEN));
+      const float u1 = ((float)(h >> 40) + 0.5f) * (1.0f / 16777216.0f);
+      const float u2 = (float)((h >> 16) & 0xFFFFFFull) * (1.0f / 16777216.0f);
+      val = sqrtf(-2.0f * __logf(u1)) * __cosf(6.283185307179586f * u2);
+    }
+    out[e] = val;
+  }
+}
+
 }  // namespace
 }  // namespace rg
 
@@ -186,4 +209,13 @@ extern "C" int rg_fill_seeds(const int32_t* d_perm, int64_t n_perm, int32_t batc
                                                          d_nseeds, seed_cap, s0, (uint64_t)epoch,
                                                          d_rng);
   return check_launch("fill_seeds");
+}
+
+extern "C" int rg_fill_features(const int32_t* d_ids, int64_t n, int32_t d, int32_t stride,
+                                uint64_t seed, float* d_out, void* stream) {
+  RG_REQUIRE(n >= 0 && d >= 1 && stride >= d, "rg_fill_features: bad sizes");
+  if (n == 0) return RG_OK;
+  fill_features_kernel<<<kNumSMs * 8, 256, 0, (cudaStream_t)stream>>>(d_ids, n, d, stride, seed,
+                                                                       d_out);
+  return check_launch("fill_features");
 }
