@@ -20,11 +20,21 @@ namespace {
 
 constexpr int kGatherWarps = 8;
 constexpr int kUnroll = 8;
+#ifndef RG_UNROLL_PEER
+#define RG_UNROLL_PEER 8
+#endif
+constexpr int kUnrollPeer = RG_UNROLL_PEER;  // loads in flight per lane, peer path
 
 struct Bases {
   const float* p[16];
 };
 
+// kRowAligned (used when some shards live on peer GPUs): one row (or a
+// 32-vector slice of one) per warp instruction, so every load is a single
+// row-local segment — NVLink peer reads of 400-B rows run ~12 % faster that
+// way (tools/nvlink_probe.py) while HBM-local rows prefer the flattened
+// all-lanes-busy mapping of the default instantiation.
+template <bool kRowAligned>
 __global__ void __launch_bounds__(kGatherWarps * 32, 4)
     gather_bundle_kernel(const int32_t* __restrict__ ids, const int32_t* __restrict__ nids,
                          int64_t cap, const uint32_t* __restrict__ route, const __grid_constant__ Bases bases,
@@ -65,6 +75,32 @@ __global__ void __launch_bounds__(kGatherWarps * 32, 4)
     if (bp) src = bp + (int64_t)(rt & RG_ROW_MASK) * src_stride;
     const unsigned long long srcu = reinterpret_cast<unsigned long long>(src);
     float4* dst = reinterpret_cast<float4*>(out + ((int64_t)b * cap + r0) * stride);
+    if (kRowAligned) {
+      constexpr int kU = kUnrollPeer;
+      const int chunks = (nvec + 31) >> 5;
+      const int items = nr * chunks;
+      for (int i0 = 0; i0 < items; i0 += kU) {
+        float4 v[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int it = i0 + u;
+          const int rr = chunks == 1 ? it : it / chunks;
+          const int c = (it - rr * chunks) * 32 + lane;
+          const unsigned long long sp = __shfl_sync(kFull, srcu, rr & 31);
+          v[u] = (it < items && c < nvec && sp)
+                     ? ld_stream(reinterpret_cast<const float4*>(sp) + c)
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int it = i0 + u;
+          const int rr = chunks == 1 ? it : it / chunks;
+          const int c = (it - rr * chunks) * 32 + lane;
+          if (it < items && c < nvec) st_stream(dst + rr * nvec + c, v[u]);
+        }
+      }
+      continue;
+    }
     const int total = nr * nvec;
     // lane handles flattened vectors e = lane, lane+32, ...: row e/nvec, col e%nvec
     int er = lane / nvec, ec = lane - (lane / nvec) * nvec;
@@ -170,16 +206,25 @@ extern "C" int rg_gather_bundle(const int32_t* d_ids, const int32_t* d_nids, int
   // grid-strides over its batch's rows).  Measured (profiles/r01_summary.md):
   // 3/SM single wave 6.39 TB/s; 4/SM (a 16-CTA second wave at G=32) 5.15;
   // 8/SM (two waves) 5.94.
-  static const int ctas_per_sm = [] {
+  // With peer (NVLink) shards the gather is latency-bound on remote reads:
+  // 6 CTAs/SM (1.5 waves) measured best at N = 2 (9,355 vs 8,930 batches/s
+  // at 3/SM; 8/SM 9,129).
+  static const int env_ctas = [] {
     const char* e = getenv("RG_GATHER_CTAS_PER_SM");
-    return e ? std::max(1, atoi(e)) : 3;
+    return e ? std::max(1, atoi(e)) : 0;
   }();
+  const int ctas_per_sm = env_ctas ? env_ctas : (peer_mask ? 6 : 3);
   const int64_t want = (cap + kGatherWarps * 32 - 1) / (kGatherWarps * 32);
   const int gx = (int)std::max<int64_t>(
       1, std::min<int64_t>(want, ((int64_t)kNumSMs * ctas_per_sm) / G));
-  gather_bundle_kernel<<<dim3(gx, G), kGatherWarps * 32, 0, (cudaStream_t)stream>>>(
-      d_ids, d_nids, cap, d_route, bases, src_stride, stride, nvec, dq, dr, my_part, peer_mask,
-      d_out, d_counters);
+  if (peer_mask != 0)
+    gather_bundle_kernel<true><<<dim3(gx, G), kGatherWarps * 32, 0, (cudaStream_t)stream>>>(
+        d_ids, d_nids, cap, d_route, bases, src_stride, stride, nvec, dq, dr, my_part, peer_mask,
+        d_out, d_counters);
+  else
+    gather_bundle_kernel<false><<<dim3(gx, G), kGatherWarps * 32, 0, (cudaStream_t)stream>>>(
+        d_ids, d_nids, cap, d_route, bases, src_stride, stride, nvec, dq, dr, my_part, peer_mask,
+        d_out, d_counters);
   return check_launch("gather_bundle");
 }
 
