@@ -176,13 +176,6 @@ class BlockSampler:
                   ptr(dst), cap_e, ptr(nedge), _cur())
         return src, dst, nedge
 
-    def check_caps(self, ngroup: int | None = None) -> None:
-        G = self.G if ngroup is None else int(ngroup)
-        nf = self.nfront[:, :G].cpu()
-        for d in range(self.L + 1):
-            if int(nf[d].max()) > self.caps[d]:
-                raise RuntimeError(f"frontier {d} overflow: {int(nf[d].max())} > {self.caps[d]}")
-
 
 def route_table(owner: np.ndarray, shard_ids: list[np.ndarray | None]) -> np.ndarray:
     """uint32 route words: owner<<28 | row of v inside its owner's shard.

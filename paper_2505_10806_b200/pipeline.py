@@ -27,11 +27,6 @@ from .sampler import SeedSchedule
 
 I32 = torch.int32
 
-# kernels launched per C-ABI call (for the gpu_launches count)
-KERNELS_PER_CALL = {"rg_fill_seeds": 1, "rg_mark_seeds": 1, "rg_bitmap_compact": 2,
-                    "rg_sample_level": 1, "rg_gather_bundle": 1}
-
-
 @dataclass
 class HotCache:
     hot_ids: torch.Tensor  # int32 ascending

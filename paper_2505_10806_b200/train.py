@@ -177,7 +177,6 @@ def _run(cfg: RunConfig) -> list[WorkerResult]:
     labels = full.labels
     rapid = cfg.mode == "rapid"
     results = []
-    pipe0 = None
     counts = None
     for p in range(k):
         pipe = WorkerPipeline(dg, store, p, train, cfg.fanouts, cfg.batch_size, cfg.s0,

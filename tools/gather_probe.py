@@ -3,7 +3,6 @@ concurrently with a sampling level (two streams)."""
 import sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
-import numpy as np
 import torch
 from paper_2505_10806_b200 import _lib
 from paper_2505_10806_b200._lib import ptr

@@ -1,9 +1,8 @@
 """NVLink probe: remote-row gather throughput of gather_bundle_kernel vs a
 contiguous peer copy (one process, 2 GPUs, peer access)."""
-import sys, time
+import sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
-import numpy as np
 import torch
 from paper_2505_10806_b200 import _lib
 from paper_2505_10806_b200.engine import bases_array, gather_bundle
