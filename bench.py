@@ -468,7 +468,13 @@ def main():
         e2e = run_e2e(pipe, g, cfg, args, world)
 
     result = None
-    check = run_check(pipe, g, cfg, S0) if (args.check and rank == 0) else None
+    check = run_check(pipe, g, cfg, S0) if args.check else None
+    if check is not None and world > 1:
+        flags = torch.tensor([int(check["blocks_bit_exact"] and check["rows_bit_exact"])],
+                             device="cuda")
+        dist.all_reduce(flags, op=dist.ReduceOp.MIN)
+        check["all_ranks_bit_exact"] = bool(flags.item())
+    e2e_rows = run_e2e_host_rows(pipe, cfg, args, world) if not args.no_e2e else None
     if rank == 0 and world == 1 and not args.no_cpu and not cfg.get("device_features"):
         hot_np = hot.cpu().numpy().astype(np.int64)
         result = cpu_baseline(cpu_state(g, book, cfg, hot_np, part), args.cpu_seconds, nb)
@@ -504,6 +510,7 @@ def main():
                      "share_of_step": gather_ms / step_ms_local,
                      "step_frac": step_bytes / (step_ms_local / 1e3) / 1e9 / peak},
         "e2e": e2e,
+        "e2e_host_rows": e2e_rows,
         "nvlink": ({"peer_rows_per_batch": peer_rows / max(1, n_batches),
                     "bytes_per_batch": peer_rows * 4 * d / max(1, n_batches),
                     "achieved_gbs": peer_rows * 4 * d / (gather_ms / 1e3) / 1e9,
@@ -556,6 +563,52 @@ def run_check(pipe, g, cfg, s0):
     rows_ok = bool(torch.equal(pipe.rows[0, : len(ids), :d], want))
     return {"batch": 0, "input_nodes": int(len(fr[-1])), "blocks_bit_exact": bool(ok),
             "rows_bit_exact": rows_ok, "oracle_s": round(time.time() - t, 1)}
+
+
+def run_e2e_host_rows(pipe, cfg, args, world):
+    """Informational: the numpy-facing drop-in returns bundle rows on the
+    host, so each group's rows (the valid |input| x d part of every slot)
+    are copied to pinned host memory on a copy stream, overlapped with the
+    next group's sampling + gather.  PCIe-bound; bytes counted exactly."""
+    import torch
+    import torch.distributed as dist
+
+    G, nb, smp = pipe.G, pipe.nb, pipe.sampler
+    d = cfg["d"]
+    n_full = max(1, nb // G)
+    steps = max(2, min(args.steps, 6))
+    host = [torch.empty((G, pipe.cap_in, d), dtype=torch.float32).pin_memory()
+            for _ in range(2)]
+    copy = torch.cuda.Stream()
+    done = [torch.cuda.Event(), torch.cuda.Event()]
+    ready = torch.cuda.Event()
+    nbytes = 0
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t = time.perf_counter()
+    for kk in range(steps):
+        i0 = (kk % n_full) * G
+        done[kk % 2].synchronize()  # host buffer free again
+        pipe.step(i0)
+        nf = smp.nfront[smp.L, :G].cpu().numpy()
+        ready.record()
+        with torch.cuda.stream(copy):
+            copy.wait_event(ready)
+            for b in range(G):
+                n = int(nf[b])
+                host[kk % 2][b, :n].copy_(pipe.rows[b, :n, :d], non_blocking=True)
+                nbytes += n * d * 4
+            done[kk % 2].record(copy)
+        torch.cuda.current_stream().wait_stream(copy)  # rows buffer reused next step
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t
+    tt = torch.tensor([wall], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    return {"value": steps * G * world / float(tt.item()), "unit": "batches/s",
+            "d2h_bytes_per_step": nbytes / steps, "steps": steps,
+            "api": "bundle rows to pinned host memory every step (numpy drop-in layout)"}
 
 
 def run_e2e(pipe, g, cfg, args, world):
