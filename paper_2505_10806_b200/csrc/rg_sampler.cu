@@ -78,11 +78,12 @@ __device__ __forceinline__ int select_positions(uint64_t nk, int D, int T) {
 // D <= 32 < ... : the take smallest of (at most) 32 distinct keys, one per
 // lane, by an MSB-first radix select on ballots; returns the lane mask.
 // Distinct keys make it terminate after ~log2(32) informative bits.
-__device__ __forceinline__ unsigned select_mask32(uint64_t key, unsigned cand, int need) {
+__device__ __forceinline__ unsigned select_mask32(uint64_t key, unsigned cand, int need,
+                                                  int top_bit = 63) {
   unsigned sel = 0;
   const uint32_t hi = (uint32_t)(key >> 32), lo = (uint32_t)key;
 #pragma unroll 1
-  for (int bit = 63; bit >= 0; --bit) {
+  for (int bit = top_bit; bit >= 0; --bit) {
     const uint32_t w = bit >= 32 ? hi : lo;
     const unsigned ones = __ballot_sync(kFull, (w >> (bit & 31)) & 1u);
     const unsigned zeros = cand & ~ones;
@@ -164,12 +165,16 @@ __device__ __forceinline__ bool select_threshold(uint64_t nk, int D, int T, uint
   __syncwarp();
   if (count < T || count > 64) return false;
   const uint64_t k0 = lane < count ? s_key[lane] : ~0ull;
-  const uint64_t k1 = 32 + lane < count ? s_key[32 + lane] : ~0ull;
   const unsigned c0 = __ballot_sync(kFull, lane < count);
-  const unsigned c1 = __ballot_sync(kFull, 32 + lane < count);
-  unsigned s0, s1;
-  // every candidate is < t0: the bits above t0's top bit are zero for all
-  select_mask64(k0, k1, c0, c1, T, s0, s1, 63 - __clzll((long long)t0));
+  unsigned s0, s1 = 0u;
+  if (count <= 32) {
+    s0 = select_mask32(k0, c0, T, 63 - __clzll((long long)t0));  // one ballot per bit
+  } else {
+    const uint64_t k1 = 32 + lane < count ? s_key[32 + lane] : ~0ull;
+    const unsigned c1 = __ballot_sync(kFull, 32 + lane < count);
+    // every candidate is < t0: the bits above t0's top bit are zero for all
+    select_mask64(k0, k1, c0, c1, T, s0, s1, 63 - __clzll((long long)t0));
+  }
   // compact the selected candidates (already in position order) to lanes
   const int n0 = __popc(s0);
   if ((s0 >> lane) & 1u) s_pos[64 + __popc(s0 & lt)] = s_pos[lane];
