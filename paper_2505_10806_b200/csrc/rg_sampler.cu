@@ -285,7 +285,10 @@ __global__ void __launch_bounds__(kSampleWarps * 32)
       continue;
     }
     if (D <= 32) {
-      // one chunk: lane p owns position p
+      // one chunk: lane p owns position p.  The row (<= 128 B, the same
+      // sectors a selective load would touch) is loaded before the keys are
+      // computed, so its latency hides under the selection ALU work.
+      const int32_t row_nb = lane < D ? __ldg(indices + a + lane) : INT_MAX;
       unsigned sel;
       if (D <= F) {
         sel = D == 32 ? kFull : ((1u << D) - 1u);
@@ -296,7 +299,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32)
         sel = select_mask32(key, __ballot_sync(kFull, lane < D), T);
       }
       const bool mine = (sel >> lane) & 1u;
-      int32_t nb = mine ? __ldg(indices + a + lane) : INT_MAX;
+      int32_t nb = mine ? row_nb : INT_MAX;
       if (sorted_rows) {
         // ascending CSR row: position order is id order
         if (mine) {
