@@ -171,11 +171,13 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(kernel: str):
+def ncu_traffic(kernel: str, workload: str, group: int):
+    """DRAM bytes per launch from the committed ncu capture of exactly this
+    workload and group size (profiles/traffic.json), else None."""
     p = ROOT / "profiles" / "traffic.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return d.get(kernel)
+        return d.get(f"{workload}/G{group}", {}).get(kernel)
     return None
 
 
@@ -505,7 +507,7 @@ def main():
                             else (feat_bytes / 1e6, float(rows_b.mean()) * d * 4 / 1e6))},
         "roofline": {"kernel": "gather_bundle_kernel", "bound": "hbm", "achieved": achieved,
                      "peak": peak, "peak_source": peak_src, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": ncu_traffic("gather_bundle_kernel"),
+                     "frac": achieved / peak, "traffic": ncu_traffic("gather_bundle_kernel", args.config, G),
                      "bytes_per_launch": gather_bytes / args.steps,
                      "share_of_step": gather_ms / step_ms_local,
                      "step_frac": step_bytes / (step_ms_local / 1e3) / 1e9 / peak},
