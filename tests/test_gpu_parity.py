@@ -560,3 +560,34 @@ def test_training_mode_equivalence(rg, golden):
         for pa, pb in zip(ra.params, rb.params):
             assert torch.equal(pa.w_self, pb.w_self) and torch.equal(pa.w_neigh, pb.w_neigh)
             assert torch.equal(pa.bias, pb.bias)
+
+
+def test_two_gpu_peer_gather_bit_exact():
+    """One process per GPU, peer shards over NVLink (CUDA IPC): batch 0 of
+    every rank bit-exact (blocks and rows, including peer-read rows) and the
+    epoch accounting unchanged.  Needs >= 2 GPUs; skipped otherwise."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    root = Path(__file__).resolve().parents[1]
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(root / "bench.py"),
+           "--gpus", "2", "--steps", "2", "--warmup", "1", "--no-cpu", "--no-e2e", "--check"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=root,
+                         env=dict(os.environ))
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([x for x in out.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["check"]["all_ranks_bit_exact"] is True
+    assert line["remote_rows_epoch"]["uncached"] == 933_549_256
+    assert line["remote_rows_epoch"]["rpcs"] == 11_725
+    assert line["nvlink"]["peer_rows_per_batch"] > 0
