@@ -66,6 +66,9 @@ def parse():
     ap.add_argument("--nvtx", action="store_true", help="NVTX range 'timed' around the timed steps")
     ap.add_argument("--serial", action="store_true",
                     help="no sample/gather overlap (one stream, per-kernel timing)")
+    ap.add_argument("--staged", action="store_true",
+                    help="N>1: owners stage their rows per 32-row chunk and consumers read "
+                         "them contiguously (measured slower than random pulls; DESIGN.md §9)")
     ap.add_argument("--graphs", action="store_true",
                     help="replay each group's launches from a captured CUDA graph (serial)")
     return ap.parse_args()
@@ -352,8 +355,14 @@ def main():
     n_full = max(1, nb // G)
     smp = pipe.sampler
 
+    staged = world > 1 and args.staged
+    if staged:
+        pipe.enable_staging(rank, world)
+
     def step(kk, timed_events=None):
         i0 = (kk % n_full) * G
+        if staged:
+            return i0, pipe.step_staged(i0, dist.barrier, timed_events)
         if args.graphs:
             return i0, pipe.step_graph(i0)
         if not args.serial:
@@ -415,7 +424,7 @@ def main():
             torch.cuda.nvtx.range_pop()
     step_ms_local = (sum(a.elapsed_time(b) for a, b in sev) if flush
                      else start.elapsed_time(end))
-    if args.serial and not args.graphs:
+    if staged or (args.serial and not args.graphs):
         gather_ms = sum(a.elapsed_time(b) for a, b in gev)
     else:
         # overlapped run: time the gather alone on the same batches (serial)
@@ -467,7 +476,7 @@ def main():
     # e2e: host seeds in (pinned H2D), accounting out (D2H) per group
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(pipe, g, cfg, args, world)
+        e2e = run_e2e(pipe, g, cfg, args, world, staged)
 
     result = None
     check = run_check(pipe, g, cfg, S0) if args.check else None
@@ -613,7 +622,7 @@ def run_e2e_host_rows(pipe, cfg, args, world):
             "api": "bundle rows to pinned host memory every step (numpy drop-in layout)"}
 
 
-def run_e2e(pipe, g, cfg, args, world):
+def run_e2e(pipe, g, cfg, args, world, staged=False):
     """Public pipeline API with host buffers: each step copies the group's
     seed ids + batch seeds from pinned host memory (H2D), samples and
     gathers, and reads the per-batch accounting back (D2H, host-visible
@@ -643,11 +652,18 @@ def run_e2e(pipe, g, cfg, args, world):
     def one(kk):
         s = kk % n_full
         i0 = s * G
-        smp.seeds.copy_(seeds_h[s], non_blocking=True)
-        smp.nseeds.copy_(nseeds_h[s], non_blocking=True)
-        smp.rng.copy_(rng_h[s], non_blocking=True)
-        smp.run(G)
-        pipe.gather(G, i0)
+        if staged:
+            tgt = pipe.samplers[pipe.k % 2 % pipe.nbuf]
+            tgt.seeds.copy_(seeds_h[s], non_blocking=True)
+            tgt.nseeds.copy_(nseeds_h[s], non_blocking=True)
+            tgt.rng.copy_(rng_h[s], non_blocking=True)
+            pipe.step_staged(i0, dist.barrier, fill=False)
+        else:
+            smp.seeds.copy_(seeds_h[s], non_blocking=True)
+            smp.nseeds.copy_(nseeds_h[s], non_blocking=True)
+            smp.rng.copy_(rng_h[s], non_blocking=True)
+            smp.run(G)
+            pipe.gather(G, i0)
         out_h.copy_(pipe.counters[i0:i0 + G], non_blocking=True)
         torch.cuda.current_stream().synchronize()
         return int(out_h[:, 2].sum())

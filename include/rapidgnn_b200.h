@@ -180,6 +180,26 @@ int rg_gather_bundle(const int32_t* d_ids, const int32_t* d_nids, int64_t cap, i
                      int32_t stride, int32_t my_part, uint32_t peer_mask, float* d_out,
                      uint32_t* d_counters, void* stream);
 
+/* Staged multi-GPU mode.  Owner side: rows of the G slots whose route kind
+ * is in mine_mask (the partitions this GPU holds, cached by consumers or
+ * not) are copied to d_stage at their chunk-aligned slot
+ * (b*cap + 32*w + k), k = rank of the row among chunk w's rows owned by
+ * this GPU.  Consumer side: like rg_gather_bundle, but fallback rows owned
+ * by a partition on another GPU (peer_mask) are read from that GPU's
+ * staging buffer (h_stage[rank], IPC-mapped) at the same slot, so NVLink
+ * reads are contiguous runs instead of random 400-B rows.  h_rank_of[16]:
+ * partition -> rank; d_owner: uint8 partition of every node.  The caller
+ * orders "all owners staged" before the consumer gather (host barrier).  */
+int rg_stage_rows(const int32_t* d_ids, const int32_t* d_nids, int64_t cap, int32_t G,
+                  const uint32_t* d_base_route, const float* const* h_bases, uint32_t mine_mask,
+                  int32_t src_stride, int32_t stride, float* d_stage, void* stream);
+int rg_gather_bundle_staged(const int32_t* d_ids, const int32_t* d_nids, int64_t cap, int32_t G,
+                            const uint32_t* d_route, const uint8_t* d_owner,
+                            const float* const* h_bases, const float* const* h_stage,
+                            const uint8_t* h_rank_of, int32_t my_rank, int32_t src_stride,
+                            int32_t stride, int32_t my_part, uint32_t peer_mask, float* d_out,
+                            uint32_t* d_counters, void* stream);
+
 /* Same contract, rows moved by TMA bulk copies (global -> smem -> global),
  * one warp per CTA, ctas_per_sm CTAs per SM (<= 0: default 4): in-flight
  * bytes live in shared memory, so the sampler can run concurrently on the

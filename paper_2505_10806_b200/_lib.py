@@ -58,6 +58,9 @@ _SIGNATURES = {
     "rg_route_with_cache": (c_int32, [P, c_int64, P, c_int64, P, P]),
     "rg_gather_bundle": (c_int32, [P, P, c_int64, c_int32, P, P, c_int32, c_int32, c_int32,
                                    c_uint32, P, P, P]),
+    "rg_stage_rows": (c_int32, [P, P, c_int64, c_int32, P, P, c_uint32, c_int32, c_int32, P, P]),
+    "rg_gather_bundle_staged": (c_int32, [P, P, c_int64, c_int32, P, P, P, P, P, c_int32, c_int32,
+                                          c_int32, c_int32, c_uint32, P, P, P]),
     "rg_gather_bundle_tma": (c_int32, [P, P, c_int64, c_int32, P, P, c_int32, c_int32, c_int32,
                                        P, P, c_int32, P]),
     "rg_sage_mean_fwd": (c_int32, [P, c_int64, c_int32, c_int32, P, P, c_int64, P, P, c_int32, P,

@@ -17,6 +17,18 @@ import numpy as np
 
 from . import _lib
 
+_opened: dict = {}  # (rank, handle bytes) -> base address (one mapping per allocation)
+
+
+def _open(rank: int, hb: bytes) -> int:
+    key = (rank, hb)
+    if key not in _opened:
+        p = ctypes.c_void_p()
+        buf = np.frombuffer(hb, dtype=np.uint8).copy()
+        _lib.call("rg_ipc_open", buf.ctypes.data, ctypes.byref(p))
+        _opened[key] = int(p.value)
+    return _opened[key]
+
 
 def placement(k: int, world: int) -> dict[int, int]:
     """partition q -> rank holding its shard."""
@@ -50,12 +62,34 @@ def open_peer_shards(store, gathered: list[dict], rank: int) -> list[int]:
         for q, (hb, off) in handles.items():
             if store.shards[q] is not None:
                 continue
-            p = ctypes.c_void_p()
-            buf = np.frombuffer(hb, dtype=np.uint8).copy()
-            _lib.call("rg_ipc_open", buf.ctypes.data, ctypes.byref(p))
-            opened.append(int(p.value))
-            store.set_shard(q, None, base=int(p.value) + off)
+            base = _open(r, hb)
+            opened.append(base)
+            store.set_shard(q, None, base=base + off)
     return opened
+
+
+def exchange_buffers(tensors: list, rank: int, world: int) -> list[list[int]]:
+    """Map every rank's buffers: returns ptrs[i][r] = address of rank r's
+    tensors[i] in this process (own entries are the local addresses)."""
+    import torch.distributed as dist
+
+    mine = []
+    for t in tensors:
+        h = np.zeros(64, dtype=np.uint8)
+        off = np.zeros(1, dtype=np.int64)
+        _lib.call("rg_ipc_handle", t.data_ptr(), h.ctypes.data, off.ctypes.data)
+        mine.append((h.tobytes(), int(off[0])))
+    gathered: list = [None] * world
+    dist.all_gather_object(gathered, mine)
+    out = [[0] * world for _ in tensors]
+    for i, t in enumerate(tensors):
+        for r in range(world):
+            if r == rank:
+                out[i][r] = t.data_ptr()
+                continue
+            hb, off = gathered[r][i]
+            out[i][r] = _open(r, hb) + off
+    return out
 
 
 def exchange_shards(store, rank: int, world: int) -> list[int]:

@@ -144,6 +144,68 @@ class WorkerPipeline:
         gr.replay()
         return ng
 
+    def enable_staging(self, rank: int, world: int) -> None:
+        """Staged multi-GPU mode (rg_stage_rows / rg_gather_bundle_staged):
+        two chunk-aligned staging buffers, mapped on every rank."""
+        from . import multigpu
+
+        st = self.store
+        self.rank, self.world = rank, world
+        self.staging = [torch.empty((self.G, self.cap_in, st.stride), dtype=torch.float32,
+                                    device=self.dg.device) for _ in range(2)]
+        self.stage_ptrs = multigpu.exchange_buffers(self.staging, rank, world)
+        self.mine_mask = sum(1 << q for q in range(st.k) if q % world == rank)
+        rank_of = np.zeros(16, dtype=np.uint8)
+        rank_of[: st.k] = [q % world for q in range(st.k)]
+        self.rank_of = rank_of
+
+    def stage(self, ng: int, smp, slot: int) -> None:
+        """Owner side: this GPU's rows of the group into staging[slot]."""
+        st = self.store
+        _lib.call("rg_stage_rows", ptr(smp.front[smp.L]), ptr(smp.nfront[smp.L]), self.cap_in, ng,
+                  ptr(st.route), bases_array(st.bases).ctypes.data, self.mine_mask,
+                  st.src_stride, st.stride, ptr(self.staging[slot]), _lib.stream_handle())
+
+    def gather_staged(self, ng: int, i0: int, smp, slot: int, rows) -> None:
+        """Consumer side: peer rows from the owners' staging[slot]."""
+        st = self.store
+        route = st.route
+        b = list(st.bases)
+        if self.cache is not None and self.cache.hot_ids.numel():
+            b[_lib.RG_KIND_CACHE] = self.cache.rows.data_ptr()
+            route = self.cache.route
+        stage = np.zeros(8, dtype=np.uint64)
+        stage[: self.world] = self.stage_ptrs[slot]
+        _lib.call("rg_gather_bundle_staged", ptr(smp.front[smp.L]), ptr(smp.nfront[smp.L]),
+                  self.cap_in, ng, ptr(route), ptr(st.owner), bases_array(b).ctypes.data,
+                  stage.ctypes.data, self.rank_of.ctypes.data, self.rank, st.src_stride, st.stride,
+                  self.my_part, st.peer_mask, ptr(rows),
+                  ptr(self.counters) + i0 * _lib.RG_NCOUNTERS * 4, _lib.stream_handle())
+
+    def step_staged(self, i0: int, barrier, events=None, fill: bool = True) -> int:
+        """Sample, stage this GPU's rows of the group, barrier (every owner
+        staged), then gather with peer rows read from the owners' staging
+        buffers.  Buffers alternate per step; the synchronize before the
+        barrier also guarantees the previous step's readers are done.
+        fill=False: the caller already placed the group's seeds."""
+        ng = min(self.G, self.nb - i0)
+        slot = self.k % 2
+        self.k += 1
+        smp = self.samplers[slot % self.nbuf]
+        if fill:
+            self.plan.fill(self.perm, self.epoch, i0, ng, smp)
+        smp.run(ng)
+        self.stage(ng, smp, slot)
+        torch.cuda.current_stream().synchronize()
+        barrier()
+        if events is not None:
+            events[0].record()
+        self.gather_staged(ng, i0, smp, slot, self.row_bufs[slot % self.nbuf])
+        if events is not None:
+            events[1].record()
+        self.launches += 1 + 1 + 2 + smp.L * 3 + 2
+        return ng
+
     def step_overlapped(self, i0: int) -> int:
         """Like step(), but sampling and gather of consecutive groups overlap
         on two streams (buffer k % nbuf).  Call sync_streams() before reading
