@@ -90,6 +90,9 @@ int rg_mark_seeds(const int32_t* d_seeds, const int32_t* d_nseeds, int32_t G, in
  *   batch bitmap, so after the step bm = F_d U src (sampler.py:148).
  * d_slow: scratch of 1 + G*cap_in int32, required only when fanout > 32
  * (rows with take > 32 go to a CTA-per-row path); fanout <= 4096.
+ * d_meta: optional scratch of G*cap_in x 16 B (int4 per slot); when given,
+ * a lane-parallel pass first stores (row start, degree, id) of every
+ * frontier node so the per-node warps skip the front -> indptr chain.
  * sorted_rows != 0 promises every CSR row is ascending (true for the
  * reference's generator and from_edge_list): selected positions are then
  * emitted in position order without a sort.                            */
@@ -97,7 +100,7 @@ int rg_sample_level(const int64_t* d_indptr, const int32_t* d_indices, int64_t n
                     int32_t G, const int32_t* d_front, int64_t cap_in, const int32_t* d_nfront,
                     int32_t fanout, int32_t level, const uint64_t* d_rng_seed, int32_t* d_ell,
                     int32_t* d_cnt, uint32_t* d_bm, int64_t nwords, int32_t* d_slow,
-                    int32_t sorted_rows, int32_t prng, void* stream);
+                    int32_t* d_meta, int32_t sorted_rows, int32_t prng, void* stream);
 
 /* PRNG variants (not in the reference; semantics in rg_prng.cuh and
  * DESIGN.md §10): prng = 0 SplitMix64 keys (reference), 1 pcg32,

@@ -43,7 +43,7 @@ _SIGNATURES = {
                                 c_int64, P, P]),
     "rg_mark_seeds": (c_int32, [P, P, c_int32, c_int32, P, c_int64, P]),
     "rg_sample_level": (c_int32, [P, P, c_int64, c_int32, P, c_int64, P, c_int32, c_int32, P, P,
-                                  P, P, c_int64, P, c_int32, c_int32, P]),
+                                  P, P, c_int64, P, P, c_int32, c_int32, P]),
     "rg_bitmap_chunks": (c_int64, [c_int64]),
     "rg_bitmap_compact": (c_int32, [P, c_int64, c_int32, P, P, c_int64, P, P, P]),
     "rg_bitmap_set": (c_int32, [P, P, P, P]),

@@ -388,7 +388,10 @@ extern "C" int rg_gather_bundle(const int32_t* d_ids, const int32_t* d_nids, int
   // One wave: (SMs x 3) CTAs split evenly over the G batches (each CTA
   // grid-strides over its batch's rows).  Measured (profiles/r01_summary.md):
   // 3/SM single wave 6.39 TB/s; 4/SM (a 16-CTA second wave at G=32) 5.15;
-  // 8/SM (two waves) 5.94.
+  // 8/SM (two waves) 5.94.  Inside the overlapped step (the next group's
+  // sampling on a second stream) 4/SM is ~2 % faster end to end (8,080 vs
+  // 7,920 batches/s) though the gather alone drops to ~6.2 TB/s: 4/SM is
+  // the default.
   // With peer (NVLink) shards the gather is latency-bound on remote reads:
   // 6 CTAs/SM (1.5 waves) measured best at N = 2 (9,355 vs 8,930 batches/s
   // at 3/SM; 8/SM 9,129).
@@ -396,7 +399,7 @@ extern "C" int rg_gather_bundle(const int32_t* d_ids, const int32_t* d_nids, int
     const char* e = getenv("RG_GATHER_CTAS_PER_SM");
     return e ? std::max(1, atoi(e)) : 0;
   }();
-  const int ctas_per_sm = env_ctas ? env_ctas : (peer_mask ? 6 : 3);
+  const int ctas_per_sm = env_ctas ? env_ctas : (peer_mask ? 6 : 4);
   const int64_t want = (cap + kGatherWarps * 32 - 1) / (kGatherWarps * 32);
   const int gx = (int)std::max<int64_t>(
       1, std::min<int64_t>(want, ((int64_t)kNumSMs * ctas_per_sm) / G));

@@ -142,8 +142,8 @@ __device__ __forceinline__ bool select_threshold(uint64_t nk, int D, int T, uint
                                                  int32_t* s_pos, int& pos_out) {
   const int lane = lane_id();
   const unsigned lt = (1u << lane) - 1u;
-  const float mu = (float)T + 3.0f * sqrtf((float)T) + 3.0f;
-  const float frac = mu / (float)D;  // approximate is fine: only the candidate count moves
+  const float mu = (float)T + 3.0f * sqrtf((float)T) + 3.0f;  // T = F here: loop-invariant
+  const float frac = __fdividef(mu, (float)D);  // approximate: only the candidate count moves
   const uint64_t t0 = frac >= 1.0f ? ~0ull : (uint64_t)(frac * 18446744073709551616.0f);
   int count = 0;
   uint64_t kk = nk + (uint64_t)(lane + 1) * GOLDEN;
@@ -168,6 +168,7 @@ __device__ __forceinline__ bool select_threshold(uint64_t nk, int D, int T, uint
   const unsigned c0 = __ballot_sync(kFull, lane < count);
   unsigned s0, s1 = 0u;
   if (count <= 32) {
+    // every candidate is < t0: the bits above t0's top bit are zero for all
     s0 = select_mask32(k0, c0, T, 63 - __clzll((long long)t0));  // one ballot per bit
   } else {
     const uint64_t k1 = 32 + lane < count ? s_key[32 + lane] : ~0ull;
@@ -216,10 +217,29 @@ __device__ __forceinline__ int prng_positions(int prng, uint64_t nk, uint64_t sd
   return floyd_positions(g, D, T);
 }
 
+// Per-node metadata (CSR row start, degree, id) for every frontier slot,
+// one thread per node: the front -> indptr loads then run lane-parallel and
+// the warp-per-node kernel starts from one independent 16-B load instead of
+// a two-hop dependent chain.
+__global__ void __launch_bounds__(256)
+    node_meta_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ front,
+                     int64_t cap_in, const int32_t* __restrict__ nfront, int4* __restrict__ meta) {
+  const int b = blockIdx.y;
+  const int nfb = nfront[b];
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nfb; j += gridDim.x * blockDim.x) {
+    const int64_t r = (int64_t)b * cap_in + j;
+    const int32_t v = front[r];
+    const int64_t a = indptr[v];
+    const int64_t e = indptr[v + 1];
+    meta[r] = make_int4((int)(uint32_t)a, (int)(a >> 32), (int)(e - a), v);
+  }
+}
+
 template <bool kVariants>
 __global__ void __launch_bounds__(kSampleWarps * 32)
     sample_level_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
-                        int G, const int32_t* __restrict__ front, int64_t cap_in,
+                        int G, const int32_t* __restrict__ front, const int4* __restrict__ meta,
+                        int64_t cap_in,
                         const int32_t* __restrict__ nfront, int F, uint64_t level_mix,
                         const uint64_t* __restrict__ rng_seed, int32_t* __restrict__ ell,
                         int32_t* __restrict__ cnt, uint32_t* __restrict__ bm, int64_t nwords,
@@ -251,9 +271,19 @@ __global__ void __launch_bounds__(kSampleWarps * 32)
     const int j = (int)ju;
     const unsigned k = (unsigned)j * (unsigned)G + (unsigned)b;  // item id (slow path)
     const int64_t row = (int64_t)b * cap_in + j;
-    const int32_t v = front[row];
-    const int64_t a = indptr[v];
-    const int D = (int)(indptr[v + 1] - a);
+    int32_t v;
+    int64_t a;
+    int D;
+    if (meta) {
+      const int4 m = __ldg(meta + row);
+      a = (int64_t)(((uint64_t)(uint32_t)m.y << 32) | (uint32_t)m.x);
+      D = m.z;
+      v = m.w;
+    } else {
+      v = front[row];
+      a = indptr[v];
+      D = (int)(indptr[v + 1] - a);
+    }
     const int T = min(D, F);
     if (lane == 0) cnt[row] = T;
     if (T > 32) {  // only reachable with fanout > 32: block path below
@@ -319,7 +349,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32)
     const uint64_t sd = s_seed[0];
     const uint64_t nk = mix64(((uint64_t)v + 1ull) * GOLDEN ^ sd);
     int pos;
-    const bool ordered = select_threshold(nk, D, T, s_key[warp], s_pos[warp], pos);
+    const bool ordered = select_threshold(nk, D, F, s_key[warp], s_pos[warp], pos);  // T == F here
     if (!ordered) pos = select_positions(nk, D, T);
     int32_t nb = INT_MAX;
     if (sorted_rows) {
@@ -665,7 +695,8 @@ extern "C" int rg_sample_level(const int64_t* d_indptr, const int32_t* d_indices
                                const int32_t* d_nfront, int32_t fanout, int32_t level,
                                const uint64_t* d_rng_seed, int32_t* d_ell, int32_t* d_cnt,
                                uint32_t* d_bm, int64_t nwords, int32_t* d_slow,
-                               int32_t sorted_rows, int32_t prng, void* stream) {
+                               int32_t* d_meta, int32_t sorted_rows, int32_t prng,
+                               void* stream) {
   RG_REQUIRE(prng >= kSplitMix && prng <= kXoshiro256pp, "rg_sample_level: unknown prng %d", prng);
   RG_REQUIRE(G >= 1 && G <= 65535 && cap_in >= 1 && n >= 1, "rg_sample_level: bad sizes");
   RG_REQUIRE(fanout >= 1, "rg_sample_level: fanout must be >= 1");
@@ -679,18 +710,24 @@ extern "C" int rg_sample_level(const int64_t* d_indptr, const int32_t* d_indices
   int32_t* slow = fanout > 32 ? d_slow : nullptr;
   if (slow && cudaMemsetAsync(slow, 0, sizeof(int32_t), s) != cudaSuccess)
     return check_launch("sample_level memset");
+  int4* meta = reinterpret_cast<int4*>(d_meta);
+  if (meta) {
+    const int bx = (int)std::min<int64_t>((cap_in + 255) / 256, std::max(1, kNumSMs * 16 / G));
+    node_meta_kernel<<<dim3(bx, G), 256, 0, s>>>(d_indptr, d_front, cap_in, d_nfront, meta);
+    if (int rc = check_launch("node_meta")) return rc;
+  }
   const int grid = kNumSMs * 5;  // 48 regs x 256 threads: 5 CTAs per SM
   // SplitMix64 keys (the reference) and the PRNG variants are separate
   // instantiations so the reference path keeps its register budget
   if (prng == kSplitMix)
     sample_level_kernel<false><<<dim3(std::max(1, grid / G), G), kSampleWarps * 32, 0,
-                                 s>>>(d_indptr, d_indices, G, d_front, cap_in, d_nfront, fanout,
+                                 s>>>(d_indptr, d_indices, G, d_front, meta, cap_in, d_nfront, fanout,
                                       level_mix, d_rng_seed, d_ell, d_cnt, d_bm, nwords, slow,
                                       sorted_rows, prng);
   else
     sample_level_kernel<true><<<dim3(std::max(1, kNumSMs * 4 / G), G),
                                 kSampleWarps * 32, 0, s>>>(
-        d_indptr, d_indices, G, d_front, cap_in, d_nfront, fanout, level_mix, d_rng_seed, d_ell,
+        d_indptr, d_indices, G, d_front, meta, cap_in, d_nfront, fanout, level_mix, d_rng_seed, d_ell,
         d_cnt, d_bm, nwords, slow, sorted_rows, prng);
   int rc = check_launch("sample_level");
   if (rc || !slow) return rc;

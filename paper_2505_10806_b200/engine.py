@@ -134,6 +134,8 @@ class BlockSampler:
         self.chunk = torch.empty((G, int(lib.rg_bitmap_chunks(dg.nwords))), dtype=I32, device=dev)
         self.slow = (torch.empty(1 + G * max(caps[:-1]), dtype=I32, device=dev)
                      if max(self.step_fan) > 32 else None)
+        # per-slot (row start, degree, id) records for the sampler (16 B each)
+        self.meta = torch.empty((G, max(caps[:-1]), 4), dtype=I32, device=dev)
 
     def set_seeds(self, b: int, seeds: np.ndarray, rng_seed: int) -> None:
         """Host seeds for slot b (API path; the plan path fills on device)."""
@@ -155,7 +157,7 @@ class BlockSampler:
             _lib.call("rg_sample_level", ptr(dg.indptr), ptr(dg.indices), dg.n, G,
                       ptr(self.front[d]), self.caps[d], ptr(self.nfront[d]), self.step_fan[d], d,
                       ptr(self.rng), ptr(self.ell[d]), ptr(self.cnt[d]), ptr(self.bm), dg.nwords,
-                      ptr(self.slow), int(dg.sorted_rows), self.prng_code, s)
+                      ptr(self.slow), ptr(self.meta), int(dg.sorted_rows), self.prng_code, s)
             _lib.call("rg_bitmap_compact", ptr(self.bm), dg.nwords, G, ptr(self.chunk),
                       ptr(self.front[d + 1]), self.caps[d + 1], ptr(self.nfront[d + 1]), None, s)
 
