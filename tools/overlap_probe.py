@@ -60,3 +60,33 @@ cur.wait_stream(sA); cur.wait_stream(sB)
 e[5].record()
 torch.cuda.synchronize()
 print(f"concurrent: gather ends {e[4].elapsed_time(ea):.3f} ms, sample ends {e[4].elapsed_time(eb):.3f} ms, both {e[4].elapsed_time(e[5]):.3f} ms")
+
+# sampling next to a register-free HBM copy (cudaMemcpyAsync D2D of ~2 GB;
+# no SM registers held): does the sampler keep its speed when HBM is busy?
+big_a = torch.empty(2 * 1024**3 // 4, dtype=torch.float32, device="cuda")
+big_b = torch.empty_like(big_a)
+for _ in range(2):
+    big_b.copy_(big_a)
+torch.cuda.synchronize()
+e0, e1 = ev(), ev()
+e0.record(); big_b.copy_(big_a); e1.record(); torch.cuda.synchronize()
+tc = e0.elapsed_time(e1)
+print(f"copy alone {tc:.3f} ms = {2 * big_a.numel() * 4 / tc / 1e6:.0f} GB/s")
+e4 = ev(); e4.record()
+sA.wait_event(e4); sB.wait_event(e4)
+with torch.cuda.stream(sA):
+    big_b.copy_(big_a); ea = ev(); ea.record(sA)
+with torch.cuda.stream(sB):
+    sample(B, 96); eb = ev(); eb.record(sB)
+torch.cuda.synchronize()
+print(f"concurrent with copy: copy ends {e4.elapsed_time(ea):.3f} ms, sample ends {e4.elapsed_time(eb):.3f} ms")
+with torch.cuda.stream(sB):
+    sample(B, 96)
+e4 = ev(); e4.record()
+sA.wait_event(e4); sB.wait_event(e4)
+with torch.cuda.stream(sB):
+    sample(B, 96); eb = ev(); eb.record(sB)
+with torch.cuda.stream(sA):
+    big_b.copy_(big_a); ea = ev(); ea.record(sA)
+torch.cuda.synchronize()
+print(f"sampler first: copy ends {e4.elapsed_time(ea):.3f} ms, sample ends {e4.elapsed_time(eb):.3f} ms")
