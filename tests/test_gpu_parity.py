@@ -467,17 +467,11 @@ def test_prng_variant_plan_and_accounting(rg):
     assert got[0]["records"][0]["nodes_pulled"] == fb
 
 
-def test_products_full_size(rg, golden):
-    """Products shape at full size: inputs hash-equal to the reference's
-    generator, a full epoch of device sampling + gather whose remote-row and
-    RPC accounting equals the survey's oracle figures (SURVEY.md §8a row 14:
-    933,549,256 rows, 11,725 RPCs for worker 0), first and last batch
-    bit-exact against the oracle, bundle rows equal to the feature rows."""
-    import hashlib
-
+@pytest.fixture(scope="module")
+def products(rg, golden):
+    """Products-shape graph (hash-pinned to the reference's generator), its
+    8-way LDG partition and the device store for worker 0."""
     from paper_2505_10806_b200.engine import DeviceGraph, FeatureStore
-    from paper_2505_10806_b200.pipeline import WorkerPipeline
-    from paper_2505_10806_b200.sampler import SeedSchedule, block_from_sampler
 
     rec = golden["generator"]["products"]
     n, m, d, c, s = rec["args"]
@@ -490,10 +484,24 @@ def test_products_full_size(rg, golden):
     dg = DeviceGraph(g.indptr, g.indices, g.num_nodes)
     store = FeatureStore(book.owner, 8, d)
     ids = [np.flatnonzero(book.owner == q) for q in range(8)]
-    feats = torch.from_numpy(g.features).cuda()
     for q in range(8):
         store.set_shard(q, FeatureStore.pad_rows(g.features[ids[q]], store.src_stride, dg.device))
     store.build_route(ids)
+    return g, dg, store
+
+
+def test_products_full_size(products):
+    """Products shape at full size: inputs hash-equal to the reference's
+    generator, a full epoch of device sampling + gather whose remote-row and
+    RPC accounting equals the survey's oracle figures (SURVEY.md §8a row 14:
+    933,549,256 rows, 11,725 RPCs for worker 0), first and last batch
+    bit-exact against the oracle, bundle rows equal to the feature rows."""
+    from paper_2505_10806_b200.pipeline import WorkerPipeline
+    from paper_2505_10806_b200.sampler import SeedSchedule, block_from_sampler
+
+    g, dg, store = products
+    d = g.feat_dim
+    feats = torch.from_numpy(g.features).cuda()
     train = np.flatnonzero(g.train_mask)
     pipe = WorkerPipeline(dg, store, 0, train, [15, 10, 5], 1024, 7, 32, nbuf=1)
     sched = SeedSchedule(7, 1, pipe.nb)
@@ -520,6 +528,66 @@ def test_products_full_size(rg, golden):
     assert t["bad"] == 0
     assert t["hit"] + t["fallback"] == 933_549_256
     assert t["rpcs"] == 11_725
+
+
+def test_products_epoch_properties(products):
+    """Every batch of a full Products epoch (not just sampled ones), checked
+    on the device through size-independent properties of sample_block
+    (sampler.py:86-152) and assemble_bundle (prefetch.py:41-88):
+    take = min(deg, F); each ELL row strictly ascending (without replacement)
+    and a subset of the node's CSR row; F_{d+1} = unique(F_d U src) sorted;
+    bundle rows = the feature rows of the input nodes."""
+    from paper_2505_10806_b200.pipeline import WorkerPipeline
+    from paper_2505_10806_b200.sampler import SeedSchedule
+
+    g, dg, store = products
+    n, d = g.num_nodes, g.feat_dim
+    feats = torch.from_numpy(g.features).cuda()
+    indptr = dg.indptr
+    deg = indptr[1:] - indptr[:-1]
+    # CSR rows are ascending, so row * n + col is globally sorted
+    rowkey = (torch.repeat_interleave(torch.arange(n, device="cuda"), deg) * n
+              + dg.indices.long())
+    train = np.flatnonzero(g.train_mask)
+    pipe = WorkerPipeline(dg, store, 0, train, [15, 10, 5], 1024, 7, 32, nbuf=1)
+    pipe.start_epoch(SeedSchedule(7, 1, pipe.nb), 0)
+    smp = pipe.sampler
+    checked = 0
+    for i0 in range(0, pipe.nb, pipe.G):
+        ng = pipe.step(i0)
+        nf = smp.nfront[:, :ng].long()
+        for lv in range(smp.L):
+            F, cap = smp.step_fan[lv], smp.caps[lv]
+            ar = torch.arange(cap, device="cuda")
+            valid = ar[None, :] < nf[lv][:, None]                       # (ng, cap)
+            v = smp.front[lv][:ng].long() * valid
+            cnt = smp.cnt[lv][:ng]
+            want = torch.minimum(deg[v], torch.tensor(F, device="cuda"))
+            assert torch.equal(cnt[valid], want[valid].int()), (i0, lv)
+            ell = smp.ell[lv][:ng].view(ng, cap, F).long()
+            ev = valid[:, :, None] & (torch.arange(F, device="cuda")[None, None, :]
+                                       < cnt[:, :, None])
+            if F > 1:
+                both = ev[:, :, 1:]
+                assert bool((ell[:, :, 1:] > ell[:, :, :-1])[both].all()), (i0, lv)
+            key = (v[:, :, None] * n + ell)[ev]
+            pos = torch.searchsorted(rowkey, key).clamp_max(rowkey.numel() - 1)
+            assert torch.equal(rowkey[pos], key), (i0, lv)
+            # union: per slot offset by b * n, then one sorted unique
+            off = torch.arange(ng, device="cuda")[:, None] * n
+            cur = (v + off)[valid]
+            src = (ell + off[:, :, None])[ev]
+            uni = torch.unique(torch.cat([cur, src]))
+            valid2 = torch.arange(smp.caps[lv + 1], device="cuda")[None, :] < nf[lv + 1][:, None]
+            nxt = (smp.front[lv + 1][:ng].long() + off)[valid2]
+            assert torch.equal(uni, nxt), (i0, lv)
+        L = smp.L
+        validL = torch.arange(smp.caps[L], device="cuda")[None, :] < nf[L][:, None]
+        ids = smp.front[L][:ng].long()[validL]
+        assert torch.equal(pipe.rows[:ng, :, :d][validL], feats[ids]), i0
+        checked += ng
+    assert checked == pipe.nb
+    assert pipe.totals()["bad"] == 0
 
 
 @pytest.mark.parametrize("mode", ["rapid", "baseline"])
