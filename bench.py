@@ -275,11 +275,34 @@ def run_reference(args, cfg):
                                        f"of sample_block + assemble_bundle, one per process"},
             "e2e": {"value": value, "unit": "batches/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ---------------------------------------------------------------- B200 arm
+_JSON_OUT = None
+
+
+def _claim_stdout() -> None:
+    """The driver reads ONE JSON line from stdout: keep a private handle on
+    the real stdout for it and point fd 1 at stderr, so nothing a library
+    prints (NCCL's version banner under NCCL_DEBUG=VERSION/INFO, CUDA or
+    torch warnings) can land on stdout."""
+    global _JSON_OUT
+    if _JSON_OUT is None:
+        sys.stdout.flush()
+        _JSON_OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+        sys.stdout = sys.stderr
+
+
+def emit(line: dict) -> None:
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
+    _claim_stdout()
     args = parse()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
@@ -538,7 +561,7 @@ def main():
         "cpu_baseline": result,
         "check": check,
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     if world > 1:
         dist.destroy_process_group()
 
@@ -648,8 +671,38 @@ def run_e2e(pipe, g, cfg, args, world, staged=False):
             nseeds_h[s, b] = len(chunk)
             rng_h[s, b] = int(np.uint64(orc.batch_seed(S0, 0, i)).astype(np.int64))
     out_h = torch.zeros((G, 8), dtype=torch.int32).pin_memory()
+    overlapped = not staged and not args.serial and not args.graphs
+    ring = [torch.zeros((G, 8), dtype=torch.int32).pin_memory() for _ in range(2)]
+    ring_ev = [torch.cuda.Event() for _ in range(2)]
+    pending = []
+
+    def one_overlapped(kk):
+        """Prefetcher-style: group kk's seeds go H2D and its sample/gather
+        are enqueued, then group kk-1's accounting (enqueued D2H behind its
+        gather) is read on the host."""
+        s = kk % n_full
+        i0 = s * G
+        pipe.step_overlapped(i0, (seeds_h[s], nseeds_h[s], rng_h[s]))
+        r = kk % 2
+        with torch.cuda.stream(pipe.s_gather):
+            ring[r].copy_(pipe.counters[i0:i0 + G], non_blocking=True)
+            ring_ev[r].record(pipe.s_gather)
+        pending.append(r)
+        got = 0
+        while len(pending) > 1:
+            q = pending.pop(0)
+            ring_ev[q].synchronize()
+            got += int(ring[q][:, 2].sum())
+        return got
+
+    def drain():
+        while pending:
+            q = pending.pop(0)
+            ring_ev[q].synchronize()
 
     def one(kk):
+        if overlapped:
+            return one_overlapped(kk)
         s = kk % n_full
         i0 = s * G
         if staged:
@@ -668,15 +721,21 @@ def run_e2e(pipe, g, cfg, args, world, staged=False):
         torch.cuda.current_stream().synchronize()
         return int(out_h[:, 2].sum())
 
+    if overlapped:
+        pipe.enter_streams()
     for kk in range(args.warmup):
         one(kk)
+    drain()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     t = time.perf_counter()
     for kk in range(args.steps):
         one(args.warmup + kk)
+    drain()  # the last group's accounting is on the host inside the timed region
     wall = time.perf_counter() - t
+    if overlapped:
+        pipe.sync_streams()
     tt = torch.tensor([wall], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -685,7 +744,9 @@ def run_e2e(pipe, g, cfg, args, world, staged=False):
     d2h = G * 8 * 4
     return {"value": args.steps * G * world / wall, "unit": "batches/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "api": "WorkerPipeline: seeds from pinned host, accounting read back per step"}
+            "api": "WorkerPipeline: seeds from pinned host, accounting read back per step"
+                   + (" (prefetcher-style: step k's read-back after step k+1 is enqueued)"
+                      if overlapped else "")}
 
 
 if __name__ == "__main__":

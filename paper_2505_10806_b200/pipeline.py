@@ -206,17 +206,25 @@ class WorkerPipeline:
         self.launches += 1 + 1 + 2 + smp.L * 3 + 2
         return ng
 
-    def step_overlapped(self, i0: int) -> int:
+    def step_overlapped(self, i0: int, host_seeds=None) -> int:
         """Like step(), but sampling and gather of consecutive groups overlap
         on two streams (buffer k % nbuf).  Call sync_streams() before reading
-        results on the current stream."""
+        results on the current stream.  host_seeds = (seeds [G, cap0] int32,
+        nseeds [G] int32, batch seeds [G] int64) pinned host tensors: the
+        group's seeds are copied H2D on the sampling stream instead of being
+        filled from the device plan."""
         ng = min(self.G, self.nb - i0)
         slot = self.k % self.nbuf
         self.k += 1
         smp = self.samplers[slot]
         with torch.cuda.stream(self.s_sample):
             self.s_sample.wait_event(self.ev_gathered[slot])  # slot free again
-            self.plan.fill(self.perm, self.epoch, i0, ng, smp)
+            if host_seeds is None:
+                self.plan.fill(self.perm, self.epoch, i0, ng, smp)
+            else:
+                smp.seeds.copy_(host_seeds[0], non_blocking=True)
+                smp.nseeds.copy_(host_seeds[1], non_blocking=True)
+                smp.rng.copy_(host_seeds[2], non_blocking=True)
             smp.run(ng)
             self.ev_sampled[slot].record(self.s_sample)
         with torch.cuda.stream(self.s_gather):
