@@ -528,6 +528,7 @@ __global__ void __launch_bounds__(kCompactThreads)
   __shared__ int s_red[32];
   __shared__ int s_base;
   __shared__ int s_warp[kWarps];
+  __shared__ int32_t s_ids[kWarps][32 * 32];  // one 32-word group's ids per warp
   const int b = blockIdx.y;
   const int64_t chunk = blockIdx.x;
   const int lane = lane_id(), warp = threadIdx.x >> 5;
@@ -563,7 +564,7 @@ __global__ void __launch_bounds__(kCompactThreads)
   int at = s_base;
   for (int i = 0; i < warp; ++i) at += s_warp[i];
   int32_t* o = out + (int64_t)b * cap_out;
-  const unsigned lt = (1u << lane) - 1u;
+  int32_t* sid = s_ids[warp];
 #pragma unroll
   for (int g = 0; g < kPerWarp / 32; ++g) {
     // exclusive prefix of this group's word popcounts
@@ -574,21 +575,24 @@ __global__ void __launch_bounds__(kCompactThreads)
       const int y = __shfl_up_sync(kFull, x, s2);
       if (lane >= s2) x += y;
     }
-    const int pre = at + x - c;
     const int64_t wi = wbase + g * 32 + lane;
-    if (wpre && wi < nwords) wpre[(int64_t)b * nwords + wi] = pre;
+    if (wpre && wi < nwords) wpre[(int64_t)b * nwords + wi] = at + x - c;
     const int gsum = __shfl_sync(kFull, x, 31);
-    unsigned any = __ballot_sync(kFull, c != 0);
-    while (any) {
-      const int jw = __ffs(any) - 1;
-      any &= any - 1;
-      const uint32_t word = __shfl_sync(kFull, words[g], jw);
-      const int off = __shfl_sync(kFull, pre, jw);
-      if ((word >> lane) & 1u) {
-        const int pos = off + __popc(word & lt);
-        if (pos < cap_out) o[pos] = (int32_t)((wbase + g * 32 + jw) * 32 + lane);
-      }
+    // each lane writes its own word's ids (ascending) into the warp's run,
+    // then the run goes out with coalesced stores
+    uint32_t word = words[g];
+    int p = x - c;
+    const int32_t idbase = (int32_t)(wi * 32);
+    while (word) {
+      sid[p++] = idbase + (__ffs(word) - 1);
+      word &= word - 1u;
     }
+    __syncwarp();
+    for (int i = lane; i < gsum; i += 32) {
+      const int pos = at + i;
+      if (pos < cap_out) o[pos] = sid[i];
+    }
+    __syncwarp();
     at += gsum;
   }
 }
