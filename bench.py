@@ -34,8 +34,11 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "sample+fetch mini-batches/s, Products-shape, 1-8 B200; remote rows/epoch"
 CONFIGS = {
+    # group 64: at N > 1 a group's peer rows are prefetched once (their union
+    # is near the whole peer shard already at 32 batches), so the NVLink cost
+    # per batch halves from 32 to 64; N = 1 is indifferent (8,220 vs 8,219)
     "products": dict(n=2_449_029, m=13, d=100, classes=47, fanouts=[15, 10, 5], batch=1024,
-                     parts=8),
+                     parts=8, group=64),
     "reddit": dict(n=232_965, m=246, d=602, classes=41, fanouts=[25, 10], batch=1024, parts=8),
     "c1": dict(n=100_000, m=10, d=128, classes=8, fanouts=[10, 5], batch=1024, parts=2),
     # config X: structure / masks / partition from the bit-exact native
@@ -66,6 +69,8 @@ def parse():
     ap.add_argument("--nvtx", action="store_true", help="NVTX range 'timed' around the timed steps")
     ap.add_argument("--serial", action="store_true",
                     help="no sample/gather overlap (one stream, per-kernel timing)")
+    ap.add_argument("--pull", action="store_true",
+                    help="N>1: every batch pulls its peer rows over NVLink (no group prefetch)")
     ap.add_argument("--staged", action="store_true",
                     help="N>1: owners stage their rows per 32-row chunk and consumers read "
                          "them contiguously (measured slower than random pulls; DESIGN.md §9)")
@@ -381,6 +386,8 @@ def main():
     staged = world > 1 and args.staged
     if staged:
         pipe.enable_staging(rank, world)
+    elif world > 1 and not args.pull:
+        pipe.enable_prefetch()
 
     def step(kk, timed_events=None):
         i0 = (kk % n_full) * G
@@ -450,7 +457,11 @@ def main():
     if staged or (args.serial and not args.graphs):
         gather_ms = sum(a.elapsed_time(b) for a, b in gev)
     else:
-        # overlapped run: time the gather alone on the same batches (serial)
+        # overlapped run: time the gather alone on the same batches (serial),
+        # and the group prefetch (NVLink) on its own
+        pev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        pf0 = int(pipe.pf_rows.item()) if pipe.prefetch else 0
         for kk in range(args.steps):
             i0 = ((args.warmup + kk) % n_full) * G
             ng = min(G, nb - i0)
@@ -458,17 +469,27 @@ def main():
             smp.run(ng)
             if flush:
                 scrub.fill_(float(kk))
+            if pipe.prefetch:
+                pev[kk][0].record()
+                pipe.prefetch_group(ng, smp, 0)
+                pev[kk][1].record()
             gev[kk][0].record()
-            pipe.gather(ng, i0)
+            pipe.gather(ng, i0, prefetched=pipe.prefetch)
             gev[kk][1].record()
         torch.cuda.synchronize()
         gather_ms = sum(a.elapsed_time(b) for a, b in gev)
+        if pipe.prefetch:
+            prefetch_ms = sum(a.elapsed_time(b) for a, b in pev)
+            prefetch_rows = int(pipe.pf_rows.item()) - pf0
     t = torch.tensor([step_ms_local], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
     n_batches = len(timed_batches)
-    gpu_launches = args.steps * (1 + 1 + 2 + 3 * smp.L + 1)
+    # our kernels per step: fill_seeds, mark_seeds, 2 compaction, per level
+    # (node_meta, sample_level, 2 compaction), gather; + 5 for the group
+    # prefetch (kind bits, union, 2 compaction, row copy) when enabled
+    gpu_launches = args.steps * (5 + 4 * smp.L + (5 if pipe.prefetch else 0))
 
     # full-epoch accounting pass (remote rows/epoch, parity metric)
     pipe.start_epoch(sched, 0)
@@ -545,7 +566,20 @@ def main():
                      "step_frac": step_bytes / (step_ms_local / 1e3) / 1e9 / peak},
         "e2e": e2e,
         "e2e_host_rows": e2e_rows,
-        "nvlink": ({"peer_rows_per_batch": peer_rows / max(1, n_batches),
+        "nvlink": ({"mode": "group prefetch (rg_prefetch_rows): each group's peer rows "
+                            "copied once into local shadows, gather all-local",
+                    "prefetched_rows_per_group": prefetch_rows / args.steps,
+                    "prefetched_rows_per_batch": prefetch_rows / max(1, n_batches),
+                    "bytes_per_batch": prefetch_rows * 4 * d / max(1, n_batches),
+                    "achieved_gbs": prefetch_rows * 4 * d / (prefetch_ms / 1e3) / 1e9,
+                    "prefetch_ms_per_step": prefetch_ms / args.steps,
+                    "peer_copy_ref_gbs": 770.0,
+                    "note": "peer-shard payload bytes copied over NVLink by the group "
+                            "prefetch, timed alone; 770 GB/s = measured peer copy per "
+                            "direction (B200_PROFILING.md)"}
+                   if world > 1 and pipe.prefetch and not staged else
+                   {"mode": "staged" if staged else "per-batch pull",
+                    "peer_rows_per_batch": peer_rows / max(1, n_batches),
                     "bytes_per_batch": peer_rows * 4 * d / max(1, n_batches),
                     "achieved_gbs": peer_rows * 4 * d / (gather_ms / 1e3) / 1e9,
                     "peer_copy_ref_gbs": 770.0,

@@ -212,6 +212,21 @@ int rg_gather_bundle_tma(const int32_t* d_ids, const int32_t* d_nids, int64_t ca
                          int32_t src_stride, int32_t stride, int32_t my_part, float* d_out,
                          uint32_t* d_counters, int32_t ctas_per_sm, void* stream);
 
+/* ---- group prefetch of peer rows (north_star item 4) ---
+ * bits[w] bit j = the route kind of node 32w+j is in kind_mask.         */
+int rg_route_kind_bits(const uint32_t* d_route, int64_t n, uint32_t kind_mask, uint32_t* d_bits,
+                       void* stream);
+/* out[w] = mask[w] & OR over b < G of bm[b*nwords + w]: the group's input
+ * nodes (level-L bitmaps of rg_sample_level) that live on peer shards.  */
+int rg_group_union(const uint32_t* d_bm, int64_t nwords, int32_t G, const uint32_t* d_mask,
+                   uint32_t* d_out, void* stream);
+/* for i < *nids: copy the row of ids[i] (kind/row from its route word)
+ * from h_src[kind] to h_dst[kind] at the same row offset (src_stride
+ * floats per row, ceil(d/4) 16-B vectors): peer shard -> local shadow.  */
+int rg_prefetch_rows(const int32_t* d_ids, const int32_t* d_nids, int64_t cap,
+                     const uint32_t* d_route, const float* const* h_src, float* const* h_dst,
+                     int32_t src_stride, int32_t d, void* stream);
+
 /* ---- L5 aggregation consumer (model.py:72-81, 126-135) -------------- */
 /* mean[t] = (sum over t's edges, in stored order, of h[pos(src)]) /
  * max(cnt_t, 1) and self[t] = h[pos(dst_front[t])], positions located by

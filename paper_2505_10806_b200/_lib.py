@@ -12,6 +12,8 @@ import threading
 from ctypes import c_int32, c_int64, c_uint32, c_uint64, c_void_p
 from pathlib import Path
 
+import numpy as np
+
 _HERE = Path(__file__).resolve().parent
 LIB_PATH = _HERE / "librapidgnn_b200.so"
 
@@ -59,6 +61,9 @@ _SIGNATURES = {
     "rg_gather_bundle": (c_int32, [P, P, c_int64, c_int32, P, P, c_int32, c_int32, c_int32,
                                    c_uint32, P, P, P]),
     "rg_stage_rows": (c_int32, [P, P, c_int64, c_int32, P, P, c_uint32, c_int32, c_int32, P, P]),
+    "rg_route_kind_bits": (c_int32, [P, c_int64, c_uint32, P, P]),
+    "rg_group_union": (c_int32, [P, c_int64, c_int32, P, P, P]),
+    "rg_prefetch_rows": (c_int32, [P, P, c_int64, P, P, P, c_int32, c_int32, P]),
     "rg_gather_bundle_staged": (c_int32, [P, P, c_int64, c_int32, P, P, P, P, P, c_int32, c_int32,
                                           c_int32, c_int32, c_uint32, P, P, P]),
     "rg_gather_bundle_tma": (c_int32, [P, P, c_int64, c_int32, P, P, c_int32, c_int32, c_int32,
@@ -150,12 +155,19 @@ def device() -> ctypes.CDLL:
     return lib
 
 
+def _args(args):
+    """numpy arrays pass as their host address; the caller's args tuple
+    keeps them alive for the duration of the call (a temporary's
+    .ctypes.data taken inline would dangle once the array is freed)."""
+    return [a.ctypes.data if isinstance(a, np.ndarray) else a for a in args]
+
+
 def call(name: str, *args) -> None:
-    check(getattr(device(), name)(*args), name)
+    check(getattr(device(), name)(*_args(args)), name)
 
 
 def host_call(name: str, *args) -> None:
-    check(getattr(load(), name)(*args), name)
+    check(getattr(load(), name)(*_args(args)), name)
 
 
 def stream_handle(stream=None) -> int:

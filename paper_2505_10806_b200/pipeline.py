@@ -73,6 +73,57 @@ class WorkerPipeline:
         self.perm: torch.Tensor | None = None
         self.epoch = 0
         self.launches = 0
+        self.prefetch = False
+
+    # -- group prefetch of peer rows (multi-GPU, rg_prefetch.cu) -------------
+    def enable_prefetch(self) -> None:
+        """Serve peer-owned rows from local shadows: once a group is sampled,
+        the union of its batches' input nodes that live on peer shards is
+        copied over NVLink once (rg_group_union + compaction +
+        rg_prefetch_rows) into a local shadow of each peer shard, one shadow
+        set per buffer slot; the gather then reads only local HBM through
+        the unchanged route words (accounting identical)."""
+        st, dev = self.store, self.dg.device
+        peers = [q for q in range(st.k) if (st.peer_mask >> q) & 1]
+        self.pf_peers = peers
+        self.shadow = []
+        for _ in range(self.nbuf):
+            bufs = {q: torch.empty((int((st.owner_np == q).sum()), st.src_stride),
+                                   dtype=torch.float32, device=dev) for q in peers}
+            self.shadow.append(bufs)
+        nw = self.dg.nwords
+        lib = _lib.device()
+        self.pf_mask = torch.empty(nw, dtype=I32, device=dev)
+        self.pf_union = torch.empty(nw, dtype=I32, device=dev)
+        self.pf_chunk = torch.empty(int(lib.rg_bitmap_chunks(nw)), dtype=I32, device=dev)
+        self.pf_ids = torch.empty(st.n, dtype=I32, device=dev)
+        self.pf_n = torch.zeros(self.nbuf, dtype=I32, device=dev)
+        self.pf_rows = torch.zeros(1, dtype=torch.int64, device=dev)  # rows copied (stats)
+        self.prefetch = bool(peers)
+
+    def _route(self):
+        if self.cache is not None and self.cache.hot_ids.numel():
+            return self.cache.route
+        return self.store.route
+
+    def prefetch_group(self, ng: int, smp, slot: int) -> None:
+        """Copy the group's peer rows into shadow[slot] (current stream)."""
+        st, s = self.store, _lib.stream_handle()
+        route = self._route()
+        nw = self.dg.nwords
+        dst = [0] * 16
+        for q, t in self.shadow[slot].items():
+            dst[q] = t.data_ptr()
+        nid = ptr(self.pf_n) + 4 * slot
+        _lib.call("rg_route_kind_bits", ptr(route), st.n, st.peer_mask, ptr(self.pf_mask), s)
+        _lib.call("rg_group_union", ptr(smp.bm), nw, ng, ptr(self.pf_mask), ptr(self.pf_union), s)
+        _lib.call("rg_bitmap_compact", ptr(self.pf_union), nw, 1, ptr(self.pf_chunk),
+                  ptr(self.pf_ids), st.n, nid, None, s)
+        _lib.call("rg_prefetch_rows", ptr(self.pf_ids), nid, st.n, ptr(route),
+                  bases_array(st.bases), bases_array(dst),
+                  st.src_stride, st.stride, s)
+        self.pf_rows += self.pf_n[slot]
+        self.launches += 6
 
     # -- per epoch ---------------------------------------------------------
     def count_epoch(self, schedule: SeedSchedule, e: int) -> torch.Tensor:
@@ -96,7 +147,7 @@ class WorkerPipeline:
         if n_hot:
             nids = torch.tensor([n_hot], dtype=I32, device=self.dg.device)
             _lib.call("rg_gather_bundle", ptr(hot_ids), ptr(nids), n_hot, 1, ptr(st.route),
-                      bases_array(st.bases).ctypes.data, st.src_stride, st.src_stride, -1,
+                      bases_array(st.bases), st.src_stride, st.src_stride, -1,
                       st.peer_mask, ptr(rows), ptr(cnt), s)
         _lib.call("rg_route_with_cache", ptr(st.route), st.n, ptr(hot_ids), n_hot, ptr(route), s)
         c = cnt.cpu().numpy()[0].view(np.uint32)
@@ -163,7 +214,7 @@ class WorkerPipeline:
         """Owner side: this GPU's rows of the group into staging[slot]."""
         st = self.store
         _lib.call("rg_stage_rows", ptr(smp.front[smp.L]), ptr(smp.nfront[smp.L]), self.cap_in, ng,
-                  ptr(st.route), bases_array(st.bases).ctypes.data, self.mine_mask,
+                  ptr(st.route), bases_array(st.bases), self.mine_mask,
                   st.src_stride, st.stride, ptr(self.staging[slot]), _lib.stream_handle())
 
     def gather_staged(self, ng: int, i0: int, smp, slot: int, rows) -> None:
@@ -177,7 +228,7 @@ class WorkerPipeline:
         stage = np.zeros(8, dtype=np.uint64)
         stage[: self.world] = self.stage_ptrs[slot]
         _lib.call("rg_gather_bundle_staged", ptr(smp.front[smp.L]), ptr(smp.nfront[smp.L]),
-                  self.cap_in, ng, ptr(route), ptr(st.owner), bases_array(b).ctypes.data,
+                  self.cap_in, ng, ptr(route), ptr(st.owner), bases_array(b),
                   stage.ctypes.data, self.rank_of.ctypes.data, self.rank, st.src_stride, st.stride,
                   self.my_part, st.peer_mask, ptr(rows),
                   ptr(self.counters) + i0 * _lib.RG_NCOUNTERS * 4, _lib.stream_handle())
@@ -226,10 +277,12 @@ class WorkerPipeline:
                 smp.nseeds.copy_(host_seeds[1], non_blocking=True)
                 smp.rng.copy_(host_seeds[2], non_blocking=True)
             smp.run(ng)
+            if self.prefetch:
+                self.prefetch_group(ng, smp, slot)
             self.ev_sampled[slot].record(self.s_sample)
         with torch.cuda.stream(self.s_gather):
             self.s_gather.wait_event(self.ev_sampled[slot])
-            self.gather(ng, i0, smp, self.row_bufs[slot])
+            self.gather(ng, i0, smp, self.row_bufs[slot], slot=slot, prefetched=True)
             self.ev_gathered[slot].record(self.s_gather)
         self.launches += 1 + 1 + 2 + smp.L * 3 + 1
         return ng
@@ -245,7 +298,11 @@ class WorkerPipeline:
         cur.wait_stream(self.s_sample)
         cur.wait_stream(self.s_gather)
 
-    def gather(self, ng: int, i0: int, smp=None, rows=None) -> None:
+    def gather(self, ng: int, i0: int, smp=None, rows=None, slot: int = 0,
+               prefetched: bool = False) -> None:
+        """Bundle rows of the group sampled in smp.  With prefetch enabled,
+        peer rows come from shadow[slot] (filled here first unless the
+        caller already ran prefetch_group for this group and slot)."""
         smp = smp or self.sampler
         rows = self.rows if rows is None else rows
         st = self.store
@@ -254,9 +311,16 @@ class WorkerPipeline:
         if self.cache is not None and self.cache.hot_ids.numel():
             bases[_lib.RG_KIND_CACHE] = self.cache.rows.data_ptr()
             route = self.cache.route
+        peer_mask = st.peer_mask
+        if self.prefetch:
+            if not prefetched:
+                self.prefetch_group(ng, smp, slot)
+            for q, t in self.shadow[slot].items():
+                bases[q] = t.data_ptr()
+            peer_mask = 0  # every row is local now
         _lib.call("rg_gather_bundle", ptr(smp.front[smp.L]), ptr(smp.nfront[smp.L]), self.cap_in,
-                  ng, ptr(route), bases_array(bases).ctypes.data, st.src_stride, st.stride,
-                  self.my_part, st.peer_mask,
+                  ng, ptr(route), bases_array(bases), st.src_stride, st.stride,
+                  self.my_part, peer_mask,
                   ptr(rows), ptr(self.counters) + i0 * _lib.RG_NCOUNTERS * 4,
                   _lib.stream_handle())
 

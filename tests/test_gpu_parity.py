@@ -630,10 +630,13 @@ def test_training_mode_equivalence(rg, golden):
             assert torch.equal(pa.bias, pb.bias)
 
 
-def test_two_gpu_peer_gather_bit_exact():
-    """One process per GPU, peer shards over NVLink (CUDA IPC): batch 0 of
-    every rank bit-exact (blocks and rows, including peer-read rows) and the
-    epoch accounting unchanged.  Needs >= 2 GPUs; skipped otherwise."""
+@pytest.mark.parametrize("mode", ["prefetch", "pull"])
+def test_two_gpu_peer_gather_bit_exact(mode):
+    """One process per GPU, peer shards over NVLink (CUDA IPC), with the
+    group prefetch into local shadows (default) or per-batch peer pulls:
+    batch 0 of every rank bit-exact (blocks and rows, including rows that
+    came over NVLink) and the epoch accounting unchanged.  Needs >= 2 GPUs;
+    skipped otherwise."""
     import json
     import os
     import socket
@@ -651,6 +654,8 @@ def test_two_gpu_peer_gather_bit_exact():
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(port), str(root / "bench.py"),
            "--gpus", "2", "--steps", "2", "--warmup", "1", "--no-cpu", "--no-e2e", "--check"]
+    if mode == "pull":
+        cmd.append("--pull")
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=root,
                          env=dict(os.environ))
     assert out.returncode == 0, out.stderr[-2000:]
@@ -658,4 +663,7 @@ def test_two_gpu_peer_gather_bit_exact():
     assert line["check"]["all_ranks_bit_exact"] is True
     assert line["remote_rows_epoch"]["uncached"] == 933_549_256
     assert line["remote_rows_epoch"]["rpcs"] == 11_725
-    assert line["nvlink"]["peer_rows_per_batch"] > 0
+    if mode == "pull":
+        assert line["nvlink"]["peer_rows_per_batch"] > 0
+    else:
+        assert line["nvlink"]["prefetched_rows_per_batch"] > 0
