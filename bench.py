@@ -69,6 +69,8 @@ def parse():
     ap.add_argument("--nvtx", action="store_true", help="NVTX range 'timed' around the timed steps")
     ap.add_argument("--serial", action="store_true",
                     help="no sample/gather overlap (one stream, per-kernel timing)")
+    ap.add_argument("--timeline", action="store_true",
+                    help="stderr: per-stream event timeline of the timed overlapped steps")
     ap.add_argument("--pull", action="store_true",
                     help="N>1: every batch pulls its peer rows over NVLink (no group prefetch)")
     ap.add_argument("--staged", action="store_true",
@@ -436,6 +438,8 @@ def main():
             torch.cuda.nvtx.range_push("timed")
         start.record()
         pipe.enter_streams()
+        if args.timeline:
+            pipe.timeline = []
         for kk in range(args.steps):
             if flush:
                 pipe.sync_streams()
@@ -454,6 +458,11 @@ def main():
             torch.cuda.nvtx.range_pop()
     step_ms_local = (sum(a.elapsed_time(b) for a, b in sev) if flush
                      else start.elapsed_time(end))
+    if pipe.timeline:
+        for name, slot, e0, e1 in pipe.timeline:
+            log(f"[timeline] rank {rank} {name:8s} slot {slot} "
+                f"{start.elapsed_time(e0):9.3f} -> {start.elapsed_time(e1):9.3f} ms")
+        pipe.timeline = None
     if staged or (args.serial and not args.graphs):
         gather_ms = sum(a.elapsed_time(b) for a, b in gev)
     else:

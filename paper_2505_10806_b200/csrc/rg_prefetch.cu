@@ -12,6 +12,8 @@
 // of the group's gather; the gather then reads those rows from local HBM
 // through the unchanged route words.  Per-batch accounting (fallback rows,
 // owners, RPCs) is computed from the route words exactly as before.
+#include <cstdlib>
+
 #include "rg_common.cuh"
 
 namespace rg {
@@ -153,8 +155,16 @@ extern "C" int rg_prefetch_rows(const int32_t* d_ids, const int32_t* d_nids, int
     t.p[i] = h_dst[i];
   }
   const int nvec = (d + 3) / 4;
+  // 6 CTAs/SM (1.5 waves at 64 registers), as for the latency-bound peer
+  // gather; measured: 2/SM co-running with a split local gather pass was
+  // slower end to end
+  static const int env_ctas = [] {
+    const char* e = getenv("RG_PREFETCH_CTAS_PER_SM");
+    return e ? std::max(1, atoi(e)) : 0;
+  }();
+  const int per_sm = env_ctas ? env_ctas : 6;
   const int64_t want = (cap + 255) / 256;
-  const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)kNumSMs * 6));
+  const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)kNumSMs * per_sm));
   prefetch_rows_kernel<<<gx, 256, 0, (cudaStream_t)stream>>>(d_ids, d_nids, d_route, s, t,
                                                             src_stride, nvec);
   return check_launch("prefetch_rows");

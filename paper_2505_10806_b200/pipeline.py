@@ -74,6 +74,7 @@ class WorkerPipeline:
         self.epoch = 0
         self.launches = 0
         self.prefetch = False
+        self.timeline: list | None = None  # [(name, slot, start ev, end ev)] when set
 
     # -- group prefetch of peer rows (multi-GPU, rg_prefetch.cu) -------------
     def enable_prefetch(self) -> None:
@@ -268,8 +269,20 @@ class WorkerPipeline:
         slot = self.k % self.nbuf
         self.k += 1
         smp = self.samplers[slot]
+        tl = self.timeline
+
+        def mark(name, stream, ev=None):
+            if tl is None:
+                return None
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            if ev is not None:
+                tl.append((name, slot, ev, e))
+            return e
+
         with torch.cuda.stream(self.s_sample):
             self.s_sample.wait_event(self.ev_gathered[slot])  # slot free again
+            e0 = mark("sample", self.s_sample)
             if host_seeds is None:
                 self.plan.fill(self.perm, self.epoch, i0, ng, smp)
             else:
@@ -277,12 +290,16 @@ class WorkerPipeline:
                 smp.nseeds.copy_(host_seeds[1], non_blocking=True)
                 smp.rng.copy_(host_seeds[2], non_blocking=True)
             smp.run(ng)
+            e1 = mark("sample", self.s_sample, e0)
             if self.prefetch:
                 self.prefetch_group(ng, smp, slot)
+                mark("prefetch", self.s_sample, e1)
             self.ev_sampled[slot].record(self.s_sample)
         with torch.cuda.stream(self.s_gather):
             self.s_gather.wait_event(self.ev_sampled[slot])
+            e2 = mark("gather", self.s_gather)
             self.gather(ng, i0, smp, self.row_bufs[slot], slot=slot, prefetched=True)
+            mark("gather", self.s_gather, e2)
             self.ev_gathered[slot].record(self.s_gather)
         self.launches += 1 + 1 + 2 + smp.L * 3 + 1
         return ng
