@@ -532,7 +532,7 @@ def main():
         e2e = run_e2e(pipe, g, cfg, args, world, staged)
 
     result = None
-    check = run_check(pipe, g, cfg, S0) if args.check else None
+    check = run_check(pipe, g, cfg, S0, args.prng) if args.check else None
     if check is not None and world > 1:
         flags = torch.tensor([int(check["blocks_bit_exact"] and check["rows_bit_exact"])],
                              device="cuda")
@@ -609,10 +609,11 @@ def main():
         dist.destroy_process_group()
 
 
-def run_check(pipe, g, cfg, s0):
-    """Batch 0 of the epoch against the CPU oracle: frontiers and edges
-    bit-exact; bundle rows bit-exact against the feature rows of its input
-    nodes (re-generated / read independently of the gather)."""
+def run_check(pipe, g, cfg, s0, prng="splitmix"):
+    """Batch 0 of the epoch against the CPU oracle (the PRNG-variant oracle
+    for --prng pcg32/sfc64/xoshiro256pp): frontiers and edges bit-exact;
+    bundle rows bit-exact against the feature rows of its input nodes
+    (re-generated / read independently of the gather)."""
     import torch
 
     from oracle import gnn_oracle as orc
@@ -624,7 +625,13 @@ def run_check(pipe, g, cfg, s0):
     perm = pipe.perm[: cfg["batch"]].cpu().numpy()
     blk = block_from_sampler(smp, 0, perm, 0, 0)
     t = time.time()
-    fr, ed = orc.block(g.indptr, g.indices, perm, cfg["fanouts"], orc.batch_seed(s0, 0, 0))
+    if prng == "splitmix":
+        fr, ed = orc.block(g.indptr, g.indices, perm, cfg["fanouts"], orc.batch_seed(s0, 0, 0))
+    else:
+        from oracle import prng_oracle
+
+        fr, ed = prng_oracle.block(g.indptr, g.indices, perm, cfg["fanouts"],
+                                   orc.batch_seed(s0, 0, 0), prng)
     ok = all(np.array_equal(a, b) for a, b in zip(blk.frontiers, fr))
     ok = ok and all(np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
                     for a, b in zip(blk.edges, ed))
