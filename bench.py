@@ -572,7 +572,10 @@ def main():
                      "frac": achieved / peak, "traffic": ncu_traffic("gather_bundle_kernel", args.config, G),
                      "bytes_per_launch": gather_bytes / args.steps,
                      "share_of_step": gather_ms / step_ms_local,
-                     "step_frac": step_bytes / (step_ms_local / 1e3) / 1e9 / peak},
+                     "step_frac": step_bytes / (step_ms_local / 1e3) / 1e9 / peak,
+                     "note": ("feature table fits in L2: rows reused by the step's batches hit "
+                              "L2 (L2 is flushed only between steps), so frac can exceed 1"
+                              if flush else None)},
         "e2e": e2e,
         "e2e_host_rows": e2e_rows,
         "nvlink": ({"mode": "group prefetch (rg_prefetch_rows): each group's peer rows "
