@@ -71,6 +71,9 @@ def parse():
                     help="no sample/gather overlap (one stream, per-kernel timing)")
     ap.add_argument("--timeline", action="store_true",
                     help="stderr: per-stream event timeline of the timed overlapped steps")
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                    help="N>1 group prefetch: NVLink loads through CUDA IPC (p2p) or two "
+                         "NCCL all-to-alls, ids out and rows back (nccl; spans nodes)")
     ap.add_argument("--pull", action="store_true",
                     help="N>1: every batch pulls its peer rows over NVLink (no group prefetch)")
     ap.add_argument("--staged", action="store_true",
@@ -354,8 +357,10 @@ def main():
         else:
             store.set_shard(q, FeatureStore.pad_rows(g.features[shard_ids[q]], store.src_stride,
                                                      dg.device))
-    if world > 1:
+    if world > 1 and args.transport == "p2p":
         multigpu.exchange_shards(store, rank, world)
+    if args.transport == "nccl" and (args.pull or args.staged):
+        raise SystemExit("--transport nccl needs the group prefetch (no --pull / --staged)")
     store.build_route(shard_ids)
     train = np.flatnonzero(g.train_mask)
     group = args.group or cfg.get("group", 32)
@@ -363,6 +368,9 @@ def main():
                           nbuf=1 if (args.serial or args.graphs) else 2, prng=args.prng)
     nb, G = pipe.nb, pipe.G
     sched = SeedSchedule(S0, 1, nb)
+    staged = world > 1 and args.staged
+    if world > 1 and not args.pull and not staged:
+        pipe.enable_prefetch(args.transport, rank, world)  # before the cache fill (nccl)
 
     # per-epoch part: plan pass (access counts), hot set, cache fill
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -385,11 +393,8 @@ def main():
     n_full = max(1, nb // G)
     smp = pipe.sampler
 
-    staged = world > 1 and args.staged
     if staged:
         pipe.enable_staging(rank, world)
-    elif world > 1 and not args.pull:
-        pipe.enable_prefetch()
 
     def step(kk, timed_events=None):
         i0 = (kk % n_full) * G
@@ -578,8 +583,12 @@ def main():
                               if flush else None)},
         "e2e": e2e,
         "e2e_host_rows": e2e_rows,
-        "nvlink": ({"mode": "group prefetch (rg_prefetch_rows): each group's peer rows "
-                            "copied once into local shadows, gather all-local",
+        "nvlink": ({"mode": ("group prefetch (rg_prefetch_rows): each group's peer rows "
+                             "copied once into local shadows, gather all-local"
+                             if args.transport == "p2p" else
+                             "group prefetch over NCCL all-to-all (ids out, rows back, "
+                             "rg_scatter_rows into local shadows), gather all-local"),
+                    "transport": args.transport,
                     "prefetched_rows_per_group": prefetch_rows / args.steps,
                     "prefetched_rows_per_batch": prefetch_rows / max(1, n_batches),
                     "bytes_per_batch": prefetch_rows * 4 * d / max(1, n_batches),

@@ -227,6 +227,13 @@ int rg_prefetch_rows(const int32_t* d_ids, const int32_t* d_nids, int64_t cap,
                      const uint32_t* d_route, const float* const* h_src, float* const* h_dst,
                      int32_t src_stride, int32_t d, void* stream);
 
+/* NCCL transport of the group prefetch: rows[i] (rows_stride floats apart,
+ * received from its owner) is written to h_dst[kind] + row * dst_stride,
+ * kind/row from the route word of ids[i]; ceil(d/4) 16-B vectors.       */
+int rg_scatter_rows(const int32_t* d_ids, int64_t n, const uint32_t* d_route,
+                    const float* d_rows, int32_t rows_stride, float* const* h_dst,
+                    int32_t dst_stride, int32_t d, void* stream);
+
 /* ---- L5 aggregation consumer (model.py:72-81, 126-135) -------------- */
 /* mean[t] = (sum over t's edges, in stored order, of h[pos(src)]) /
  * max(cnt_t, 1) and self[t] = h[pos(dst_front[t])], positions located by

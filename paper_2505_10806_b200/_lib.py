@@ -64,6 +64,7 @@ _SIGNATURES = {
     "rg_route_kind_bits": (c_int32, [P, c_int64, c_uint32, P, P]),
     "rg_group_union": (c_int32, [P, c_int64, c_int32, P, P, P]),
     "rg_prefetch_rows": (c_int32, [P, P, c_int64, P, P, P, c_int32, c_int32, P]),
+    "rg_scatter_rows": (c_int32, [P, c_int64, P, P, c_int32, P, c_int32, c_int32, P]),
     "rg_gather_bundle_staged": (c_int32, [P, P, c_int64, c_int32, P, P, P, P, P, c_int32, c_int32,
                                           c_int32, c_int32, c_uint32, P, P, P]),
     "rg_gather_bundle_tma": (c_int32, [P, P, c_int64, c_int32, P, P, c_int32, c_int32, c_int32,

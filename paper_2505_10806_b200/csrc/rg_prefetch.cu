@@ -121,6 +121,42 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// rows received from their owners (NCCL transport: rows[i] belongs to
+// ids[i]) scattered into the local shadow of their shard, at the row given
+// by the route word.  Warp per 32 rows; source rows are contiguous.
+__global__ void __launch_bounds__(256)
+    scatter_rows_kernel(const int32_t* __restrict__ ids, int64_t n,
+                        const uint32_t* __restrict__ route, const float* __restrict__ rows,
+                        int rows_stride, const __grid_constant__ RowDsts dst, int dst_stride,
+                        int nvec) {
+  __shared__ float* s_dst[16];
+  if (threadIdx.x < 16) s_dst[threadIdx.x] = dst.p[threadIdx.x];
+  __syncthreads();
+  const int lane = lane_id();
+  const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5) * 32;
+  for (int64_t r0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; r0 < n;
+       r0 += wstride) {
+    const int64_t r = r0 + lane;
+    const int nr = (int)(n - r0 < 32 ? n - r0 : 32);
+    unsigned long long dp = 0;
+    if (r < n) {
+      const uint32_t rt = __ldg(route + __ldg(ids + r));
+      if (rt != RG_ROUTE_INVALID && s_dst[rt >> RG_KIND_SHIFT])
+        dp = reinterpret_cast<unsigned long long>(s_dst[rt >> RG_KIND_SHIFT] +
+                                                  (int64_t)(rt & RG_ROW_MASK) * dst_stride);
+    }
+    const float4* src = reinterpret_cast<const float4*>(rows + r0 * rows_stride);
+    const int rs4 = rows_stride / 4;
+    const int total = nr * nvec;
+    for (int e0 = 0; e0 < total; e0 += 32) {  // warp-uniform trip count
+      const int e = e0 + lane;
+      const int rr = e / nvec, c = e - rr * nvec;
+      const unsigned long long d = __shfl_sync(kFull, dp, rr & 31);
+      if (e < total && d) reinterpret_cast<float4*>(d)[c] = ld_stream(src + (int64_t)rr * rs4 + c);
+    }
+  }
+}
+
 }  // namespace
 }  // namespace rg
 
@@ -168,4 +204,21 @@ extern "C" int rg_prefetch_rows(const int32_t* d_ids, const int32_t* d_nids, int
   prefetch_rows_kernel<<<gx, 256, 0, (cudaStream_t)stream>>>(d_ids, d_nids, d_route, s, t,
                                                             src_stride, nvec);
   return check_launch("prefetch_rows");
+}
+
+extern "C" int rg_scatter_rows(const int32_t* d_ids, int64_t n, const uint32_t* d_route,
+                               const float* d_rows, int32_t rows_stride, float* const* h_dst,
+                               int32_t dst_stride, int32_t d, void* stream) {
+  RG_REQUIRE(n >= 0 && d >= 1 && rows_stride >= d && dst_stride >= d && rows_stride % 4 == 0 &&
+                 dst_stride % 4 == 0,
+             "rg_scatter_rows: bad sizes");
+  if (n == 0) return RG_OK;
+  RowDsts t;
+  for (int i = 0; i < 16; ++i) t.p[i] = h_dst[i];
+  const int64_t want = (n + 255) / 256;
+  const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)kNumSMs * 4));
+  scatter_rows_kernel<<<gx, 256, 0, (cudaStream_t)stream>>>(d_ids, n, d_route, d_rows,
+                                                            rows_stride, t, dst_stride,
+                                                            (d + 3) / 4);
+  return check_launch("scatter_rows");
 }

@@ -99,3 +99,35 @@ def exchange_shards(store, rank: int, world: int) -> list[int]:
     gathered: list = [None] * world
     dist.all_gather_object(gathered, mine)
     return open_peer_shards(store, gathered, rank)
+
+
+def exchange_rows(ids, dest, world: int, serve):
+    """Request/serve row exchange over torch.distributed (the NCCL transport of
+    the group prefetch; any backend with all_to_all_single works, gloo on CPU
+    in the tests).  The reference pulls rows per owner over TCP
+    (store.py:173-196 -> wire.py); here every rank sends each owner the ids it
+    needs in one all-to-all, owners answer with the rows in request order in a
+    second one.
+
+    ids  : 1-D int32 tensor of requested node ids (any order)
+    dest : owner rank of each id (same length)
+    serve: req_ids -> rows tensor [len(req_ids), stride] for ids this rank owns
+    Returns (send_ids, rows): rows[i] is the row of send_ids[i] (ids regrouped
+    by owner rank, stable)."""
+    import torch
+    import torch.distributed as dist
+
+    dest = dest.to(torch.int64)
+    order = torch.argsort(dest, stable=True)
+    send_ids = ids[order].contiguous()
+    counts = torch.bincount(dest, minlength=world).to(torch.int64)
+    recv_counts = torch.empty_like(counts)
+    dist.all_to_all_single(recv_counts, counts)
+    sc = [int(x) for x in counts.tolist()]
+    rc = [int(x) for x in recv_counts.tolist()]
+    req = torch.empty(sum(rc), dtype=ids.dtype, device=ids.device)
+    dist.all_to_all_single(req, send_ids, rc, sc)
+    rows = serve(req)
+    got = torch.empty((sum(sc),) + tuple(rows.shape[1:]), dtype=rows.dtype, device=rows.device)
+    dist.all_to_all_single(got, rows.contiguous(), sc, rc)
+    return send_ids, got

@@ -19,7 +19,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from . import _lib
+from . import _lib, multigpu
 from ._lib import ptr
 from .engine import BlockSampler, DeviceGraph, FeatureStore, bases_array
 from .plan import PlanPass, candidates, threshold_select
@@ -74,17 +74,32 @@ class WorkerPipeline:
         self.epoch = 0
         self.launches = 0
         self.prefetch = False
+        self.pf_transport = "p2p"
         self.timeline: list | None = None  # [(name, slot, start ev, end ev)] when set
 
     # -- group prefetch of peer rows (multi-GPU, rg_prefetch.cu) -------------
-    def enable_prefetch(self) -> None:
+    def enable_prefetch(self, transport: str = "p2p", rank: int = 0, world: int = 1) -> None:
         """Serve peer-owned rows from local shadows: once a group is sampled,
         the union of its batches' input nodes that live on peer shards is
         copied over NVLink once (rg_group_union + compaction +
         rg_prefetch_rows) into a local shadow of each peer shard, one shadow
         set per buffer slot; the gather then reads only local HBM through
-        the unchanged route words (accounting identical)."""
+        the unchanged route words (accounting identical).
+
+        transport "p2p": the copy reads the peer shard through its CUDA IPC
+        address (NVLink loads).  "nccl": the owners serve the requested rows
+        through two torch.distributed all-to-alls (ids out, rows back) and
+        they are scattered into the shadows — no peer mapping needed, so it
+        also spans nodes."""
+        if transport not in ("p2p", "nccl"):
+            raise ValueError(f"unknown transport {transport!r}")
         st, dev = self.store, self.dg.device
+        self.pf_transport, self.rank, self.world = transport, int(rank), int(world)
+        if transport == "nccl":
+            # owner rank per node; peers = shards other ranks hold
+            self.owner_rank = (st.owner.to(torch.int64) % self.world).to(torch.uint8)
+            self.nccl_peers = [q for q in range(st.k) if q % self.world != self.rank]
+            st.peer_mask = sum(1 << q for q in self.nccl_peers)
         peers = [q for q in range(st.k) if (st.peer_mask >> q) & 1]
         self.pf_peers = peers
         self.shadow = []
@@ -120,11 +135,40 @@ class WorkerPipeline:
         _lib.call("rg_group_union", ptr(smp.bm), nw, ng, ptr(self.pf_mask), ptr(self.pf_union), s)
         _lib.call("rg_bitmap_compact", ptr(self.pf_union), nw, 1, ptr(self.pf_chunk),
                   ptr(self.pf_ids), st.n, nid, None, s)
-        _lib.call("rg_prefetch_rows", ptr(self.pf_ids), nid, st.n, ptr(route),
-                  bases_array(st.bases), bases_array(dst),
-                  st.src_stride, st.stride, s)
+        if self.pf_transport == "nccl":
+            self._exchange_nccl(slot, route, dst)
+        else:
+            _lib.call("rg_prefetch_rows", ptr(self.pf_ids), nid, st.n, ptr(route),
+                      bases_array(st.bases), bases_array(dst),
+                      st.src_stride, st.stride, s)
         self.pf_rows += self.pf_n[slot]
         self.launches += 6
+
+    def _exchange_nccl(self, slot: int, route, dst) -> None:
+        """NCCL transport: requested ids to their owners, rows back, scatter
+        into shadow[slot] (current stream; one host sync for the sizes)."""
+        st = self.store
+        n = int(self.pf_n[slot].item())
+        ids = self.pf_ids[:n]
+        dest = self.owner_rank[ids.long()]
+        send_ids, rows = multigpu.exchange_rows(ids, dest, self.world, self._serve)
+        _lib.call("rg_scatter_rows", ptr(send_ids), send_ids.numel(), ptr(route), ptr(rows),
+                  st.src_stride, bases_array(dst), st.src_stride, st.src_stride,
+                  _lib.stream_handle())
+
+    def _serve(self, req):
+        """Owner side of the NCCL transport: rows (src_stride floats) of the
+        requested ids, all held by this rank's shards (base route)."""
+        st = self.store
+        out = torch.empty((max(1, req.numel()), st.src_stride), dtype=torch.float32,
+                          device=req.device)
+        if req.numel():
+            nreq = torch.tensor([req.numel()], dtype=I32, device=req.device)
+            cnt = torch.zeros((1, _lib.RG_NCOUNTERS), dtype=I32, device=req.device)
+            _lib.call("rg_gather_bundle", ptr(req), ptr(nreq), req.numel(), 1, ptr(st.route),
+                      bases_array(st.bases), st.src_stride, st.src_stride, -1, 0, ptr(out),
+                      ptr(cnt), _lib.stream_handle())
+        return out[: req.numel()]
 
     # -- per epoch ---------------------------------------------------------
     def count_epoch(self, schedule: SeedSchedule, e: int) -> torch.Tensor:
@@ -145,14 +189,25 @@ class WorkerPipeline:
         route = torch.empty_like(st.route)
         cnt = torch.zeros((1, _lib.RG_NCOUNTERS), dtype=I32, device=self.dg.device)
         s = _lib.stream_handle()
-        if n_hot:
-            nids = torch.tensor([n_hot], dtype=I32, device=self.dg.device)
-            _lib.call("rg_gather_bundle", ptr(hot_ids), ptr(nids), n_hot, 1, ptr(st.route),
-                      bases_array(st.bases), st.src_stride, st.src_stride, -1,
-                      st.peer_mask, ptr(rows), ptr(cnt), s)
         _lib.call("rg_route_with_cache", ptr(st.route), st.n, ptr(hot_ids), n_hot, ptr(route), s)
-        c = cnt.cpu().numpy()[0].view(np.uint32)
-        rpcs = bin(int(c[_lib.RG_CNT_OWNER_MASK])).count("1")
+        if self.pf_transport == "nccl":
+            # owners serve the hot rows over the all-to-all; scatter into the
+            # cache slots through the cache route (kind 15 | slot)
+            dst = [0] * 16
+            dst[_lib.RG_KIND_CACHE] = rows.data_ptr()
+            send_ids, got = multigpu.exchange_rows(hot_ids, self.owner_rank[hot_ids.long()],
+                                                   self.world, self._serve)
+            _lib.call("rg_scatter_rows", ptr(send_ids), send_ids.numel(), ptr(route), ptr(got),
+                      st.src_stride, bases_array(dst), st.src_stride, st.src_stride, s)
+            rpcs = int(torch.unique(st.owner[hot_ids.long()]).numel()) if n_hot else 0
+        else:
+            if n_hot:
+                nids = torch.tensor([n_hot], dtype=I32, device=self.dg.device)
+                _lib.call("rg_gather_bundle", ptr(hot_ids), ptr(nids), n_hot, 1, ptr(st.route),
+                          bases_array(st.bases), st.src_stride, st.src_stride, -1,
+                          st.peer_mask, ptr(rows), ptr(cnt), s)
+            c = cnt.cpu().numpy()[0].view(np.uint32)
+            rpcs = bin(int(c[_lib.RG_CNT_OWNER_MASK])).count("1")
         self.cache = HotCache(hot_ids, rows, route, (rpcs, n_hot, 4 * st.d * n_hot))
         return self.cache
 

@@ -630,10 +630,11 @@ def test_training_mode_equivalence(rg, golden):
             assert torch.equal(pa.bias, pb.bias)
 
 
-@pytest.mark.parametrize("mode", ["prefetch", "pull"])
+@pytest.mark.parametrize("mode", ["prefetch", "nccl", "pull"])
 def test_two_gpu_peer_gather_bit_exact(mode):
     """One process per GPU, peer shards over NVLink (CUDA IPC), with the
-    group prefetch into local shadows (default) or per-batch peer pulls:
+    group prefetch into local shadows (NVLink loads, or NCCL all-to-all as
+    the transport) or per-batch peer pulls:
     batch 0 of every rank bit-exact (blocks and rows, including rows that
     came over NVLink) and the epoch accounting unchanged.  Needs >= 2 GPUs;
     skipped otherwise."""
@@ -656,6 +657,8 @@ def test_two_gpu_peer_gather_bit_exact(mode):
            "--gpus", "2", "--steps", "2", "--warmup", "1", "--no-cpu", "--no-e2e", "--check"]
     if mode == "pull":
         cmd.append("--pull")
+    elif mode == "nccl":
+        cmd += ["--transport", "nccl"]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=root,
                          env=dict(os.environ))
     assert out.returncode == 0, out.stderr[-2000:]

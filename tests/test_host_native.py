@@ -253,3 +253,58 @@ def test_rgf1_rpb1_bytes_match_reference(tmp_path):
     bad.write_bytes(p.read_bytes()[:100])
     with pytest.raises(OSError):
         load_graph(bad)
+
+
+def _gloo_exchange_worker(rank, world, port, out):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2505_10806_b200.multigpu import exchange_rows
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # rank r owns ids with id % world == r; asks for a rank-dependent set
+    ids = torch.tensor([7, 2, 9, 4, 11, 0, 5] if rank == 0 else [1, 8, 3, 6, 10],
+                       dtype=torch.int32)
+    dest = ids.to(torch.int64) % world
+
+    def serve(req):
+        assert bool((req.to(torch.int64) % world == rank).all())
+        r = req.to(torch.float32)
+        return torch.stack([r * 10, r * 10 + 1, -r], dim=1)
+
+    send_ids, rows = exchange_rows(ids, dest, world, serve)
+    ok = bool(torch.equal(rows[:, 0], send_ids.to(torch.float32) * 10)) and \
+        bool(torch.equal(rows[:, 2], -send_ids.to(torch.float32)))
+    out.put((rank, ok, sorted(send_ids.tolist()) == sorted(ids.tolist()),
+             send_ids.tolist()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_two_rank_row_exchange():
+    """NCCL-transport host protocol (multigpu.exchange_rows) on 2 gloo ranks:
+    every requested id comes back with its owner's row, grouped by owner."""
+    import multiprocessing as mp
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gloo_exchange_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {r: (ok, same, order) for r, ok, same, order in (q.get(timeout=120) for _ in range(2))}
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(2):
+        ok, same, order = res[r]
+        assert ok and same
+        owners = [i % 2 for i in order]
+        assert owners == sorted(owners)  # grouped by owner rank, stable
