@@ -670,3 +670,119 @@ def test_two_gpu_peer_gather_bit_exact(mode):
         assert line["nvlink"]["peer_rows_per_batch"] > 0
     else:
         assert line["nvlink"]["prefetched_rows_per_batch"] > 0
+
+
+def test_prefetch_kernels_units(rg):
+    """K9 building blocks on one GPU: route-kind bits, masked group union,
+    row copy into shadows and the NCCL-transport scatter, against torch."""
+    from paper_2505_10806_b200 import _lib
+    from paper_2505_10806_b200.engine import bases_array
+
+    gen = torch.Generator().manual_seed(3)
+    n, G = 5000, 5
+    nw = (n + 31) // 32
+    kinds = torch.randint(0, 4, (n,), generator=gen)
+    rows_of = torch.zeros(n, dtype=torch.int64)
+    for q in range(4):
+        m = kinds == q
+        rows_of[m] = torch.arange(int(m.sum()))
+    route = ((kinds << 28) | rows_of).to(torch.int64)
+    route[::97] = 0xFFFFFFFF  # invalid words
+    route32 = torch.from_numpy(route.numpy().astype(np.uint32).view(np.int32)).cuda()
+    s = _lib.stream_handle()
+    bits = torch.empty(nw, dtype=torch.int32, device="cuda")
+    _lib.call("rg_route_kind_bits", route32.data_ptr(), n, 0b1010, bits.data_ptr(), s)
+    want = torch.zeros(nw * 32, dtype=torch.bool)
+    valid = route != 0xFFFFFFFF
+    want[:n] = valid & ((kinds == 1) | (kinds == 3))
+    got = ((bits.cpu().to(torch.int64)[:, None] >> torch.arange(32)) & 1).reshape(-1).bool()
+    assert torch.equal(got, want)
+    bm = torch.randint(-2**31, 2**31 - 1, (G, nw), generator=gen, dtype=torch.int64).to(
+        torch.int32).cuda()
+    out = torch.empty(nw, dtype=torch.int32, device="cuda")
+    _lib.call("rg_group_union", bm.data_ptr(), nw, G, bits.data_ptr(), out.data_ptr(), s)
+    ref = bm[0].clone()
+    for b in range(1, G):
+        ref |= bm[b]
+    assert torch.equal(out, ref & bits)
+    # prefetch_rows / scatter_rows: kinds 1 and 3 from "peer" shards into shadows
+    stride = 12
+    shards = {q: torch.randn((int((kinds == q).sum()), stride), generator=gen).cuda()
+              for q in range(4)}
+    ids = torch.nonzero(want[:n]).flatten().to(torch.int32).cuda()
+    nid = torch.tensor([ids.numel()], dtype=torch.int32, device="cuda")
+    src = [0] * 16
+    dst = [0] * 16
+    shadow = {}
+    for q in (1, 3):
+        src[q] = shards[q].data_ptr()
+        shadow[q] = torch.zeros_like(shards[q])
+        dst[q] = shadow[q].data_ptr()
+    _lib.call("rg_prefetch_rows", ids.data_ptr(), nid.data_ptr(), ids.numel(),
+              route32.data_ptr(), bases_array(src), bases_array(dst), stride, stride, s)
+    for q in (1, 3):
+        sel = rows_of[(kinds == q) & valid]
+        assert torch.equal(shadow[q][sel.cuda()], shards[q][sel.cuda()])
+    # scatter: rows listed in ids order land at their (kind, row)
+    perm = torch.randperm(ids.numel(), generator=gen).cuda()
+    ids_p = ids[perm].contiguous()
+    k_p = kinds[ids_p.cpu().long()]
+    r_p = rows_of[ids_p.cpu().long()]
+    payload = torch.stack([shards[int(k)][int(r)] for k, r in zip(k_p, r_p)]).cuda()
+    for q in (1, 3):
+        shadow[q].zero_()
+    _lib.call("rg_scatter_rows", ids_p.data_ptr(), ids_p.numel(), route32.data_ptr(),
+              payload.data_ptr(), stride, bases_array(dst), stride, stride, s)
+    for q in (1, 3):
+        sel = rows_of[(kinds == q) & valid]
+        assert torch.equal(shadow[q][sel.cuda()], shards[q][sel.cuda()])
+
+
+def test_group_prefetch_pipeline_single_gpu(rg, products):
+    """The whole group-prefetch path on one GPU: shards 1..7 registered as
+    'peer' addresses (set_shard(q, None, base)), so every step copies the
+    group's union into shadows and gathers all-local; bundle rows equal the
+    feature rows and the epoch accounting equals the plain pipeline's."""
+    from paper_2505_10806_b200.engine import FeatureStore
+    from paper_2505_10806_b200.pipeline import WorkerPipeline
+    from paper_2505_10806_b200.sampler import SeedSchedule
+
+    g, dg, store = products
+    d = g.feat_dim
+    book_owner = store.owner_np
+    st2 = FeatureStore(book_owner, 8, d)
+    for q in range(8):
+        if q == 0:
+            st2.set_shard(q, store.shards[0])
+        else:
+            st2.set_shard(q, None, base=store.shards[q].data_ptr())
+    st2.route = store.route
+    assert st2.peer_mask == 0b11111110
+    train = np.flatnonzero(g.train_mask)
+    feats = torch.from_numpy(g.features).cuda()
+    pipe = WorkerPipeline(dg, st2, 0, train, [15, 10, 5], 1024, 7, 16, nbuf=2)
+    pipe.enable_prefetch()
+    assert pipe.prefetch
+    sched = SeedSchedule(7, 1, pipe.nb)
+    pipe.start_epoch(sched, 0)
+    pipe.enter_streams()
+    for i0 in range(0, 8 * 16, 16):
+        pipe.step_overlapped(i0)
+    pipe.sync_streams()
+    torch.cuda.synchronize()
+    # the last group's rows (slot of step 7) against the features
+    slot = (pipe.k - 1) % pipe.nbuf
+    smp = pipe.samplers[slot]
+    nf = smp.nfront[smp.L].cpu().numpy()
+    rows = pipe.row_bufs[slot]
+    for b in (0, 7, 15):
+        ids = smp.front[smp.L][b, : nf[b]].long()
+        assert torch.equal(rows[b, : nf[b], :d], feats[ids])
+    assert int(pipe.pf_rows.item()) > 0
+    t = pipe.totals()
+    ref = WorkerPipeline(dg, store, 0, train, [15, 10, 5], 1024, 7, 16, nbuf=1)
+    ref.start_epoch(sched, 0)
+    for i0 in range(0, 8 * 16, 16):
+        ref.step(i0)
+    r = ref.totals()
+    assert t["bad"] == 0 and np.array_equal(t["per_batch"][:128, :5], r["per_batch"][:128, :5])
