@@ -128,6 +128,9 @@ __global__ void __launch_bounds__(32)
                 bp + (int64_t)(rt & RG_ROW_MASK) * src_stride, row_bytes, bar);
     } else {
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+      // invalid route word: zero row, as rg_gather_bundle writes it
+      float4* z = reinterpret_cast<float4*>(outb + r * stride);
+      for (int c = 0; c < stride / 4; ++c) z[c] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     ++L;
     if (!bp) {

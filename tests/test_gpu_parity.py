@@ -630,7 +630,7 @@ def test_training_mode_equivalence(rg, golden):
             assert torch.equal(pa.bias, pb.bias)
 
 
-@pytest.mark.parametrize("mode", ["prefetch", "nccl", "pull"])
+@pytest.mark.parametrize("mode", ["prefetch", "nccl", "pull", "staged"])
 def test_two_gpu_peer_gather_bit_exact(mode):
     """One process per GPU, peer shards over NVLink (CUDA IPC), with the
     group prefetch into local shadows (NVLink loads, or NCCL all-to-all as
@@ -659,6 +659,8 @@ def test_two_gpu_peer_gather_bit_exact(mode):
         cmd.append("--pull")
     elif mode == "nccl":
         cmd += ["--transport", "nccl"]
+    elif mode == "staged":
+        cmd.append("--staged")
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=root,
                          env=dict(os.environ))
     assert out.returncode == 0, out.stderr[-2000:]
@@ -666,7 +668,7 @@ def test_two_gpu_peer_gather_bit_exact(mode):
     assert line["check"]["all_ranks_bit_exact"] is True
     assert line["remote_rows_epoch"]["uncached"] == 933_549_256
     assert line["remote_rows_epoch"]["rpcs"] == 11_725
-    if mode == "pull":
+    if mode in ("pull", "staged"):
         assert line["nvlink"]["peer_rows_per_batch"] > 0
     else:
         assert line["nvlink"]["prefetched_rows_per_batch"] > 0
@@ -786,3 +788,49 @@ def test_group_prefetch_pipeline_single_gpu(rg, products):
         ref.step(i0)
     r = ref.totals()
     assert t["bad"] == 0 and np.array_equal(t["per_batch"][:128, :5], r["per_batch"][:128, :5])
+
+
+def test_tma_gather_matches_gather(rg):
+    """Experimental TMA bulk-copy gather (rg_gather_bundle_tma)
+    produces the same bundle rows and provenance counters as the main
+    gather, incl. cache hits, fallbacks and invalid route words."""
+    from paper_2505_10806_b200 import _lib
+    from paper_2505_10806_b200.engine import bases_array
+
+    gen = torch.Generator().manual_seed(11)
+    n, d, G, cap = 20000, 100, 3, 4000
+    kinds = torch.randint(0, 3, (n,), generator=gen)
+    kinds[torch.randperm(n, generator=gen)[:3000]] = _lib.RG_KIND_CACHE
+    rows_of = torch.zeros(n, dtype=torch.int64)
+    shards = {}
+    for q in (0, 1, 2, _lib.RG_KIND_CACHE):
+        m = kinds == q
+        rows_of[m] = torch.arange(int(m.sum()))
+        shards[q] = torch.randn((int(m.sum()), d), generator=gen).cuda()
+    route = (kinds << 28) | rows_of
+    route[::501] = 0xFFFFFFFF
+    route32 = torch.from_numpy(route.numpy().astype(np.uint32).view(np.int32)).cuda()
+    ids = torch.randint(0, n, (G, cap), generator=gen, dtype=torch.int64).to(torch.int32).cuda()
+    nids = torch.tensor([cap, cap - 17, 1], dtype=torch.int32, device="cuda")
+    b = [0] * 16
+    for q, t in shards.items():
+        b[q] = t.data_ptr()
+    bases = bases_array(b)
+    s = _lib.stream_handle()
+    outs, cnts = [], []
+    for fn in ("rg_gather_bundle", "rg_gather_bundle_tma"):
+        out = torch.full((G, cap, d), -1.0, device="cuda")
+        cnt = torch.zeros((G, _lib.RG_NCOUNTERS), dtype=torch.int32, device="cuda")
+        if fn == "rg_gather_bundle":
+            _lib.call(fn, ids.data_ptr(), nids.data_ptr(), cap, G, route32.data_ptr(), bases, d, d,
+                      0, 0, out.data_ptr(), cnt.data_ptr(), s)
+        else:
+            _lib.call(fn, ids.data_ptr(), nids.data_ptr(), cap, G, route32.data_ptr(), bases, d, d,
+                      0, out.data_ptr(), cnt.data_ptr(), 0, s)
+        outs.append(out)
+        cnts.append(cnt)
+    torch.cuda.synchronize()
+    nn = nids.cpu().tolist()
+    for g in range(G):
+        assert torch.equal(outs[0][g, : nn[g]], outs[1][g, : nn[g]]), g
+    assert torch.equal(cnts[0][:, :5], cnts[1][:, :5])
