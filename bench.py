@@ -44,7 +44,7 @@ CONFIGS = {
     # config X: structure / masks / partition from the bit-exact native
     # generator; feature rows generated on the device (rg_fill_features)
     "papers100m": dict(n=111_059_956, m=7, d=128, classes=172, fanouts=[15, 10, 5], batch=4096,
-                       parts=8, device_features=True, group=4),
+                       parts=8, device_features=True, group=8),
 }
 S0 = 7
 L2_BYTES = 126 * 2**20
