@@ -101,7 +101,7 @@ def exchange_shards(store, rank: int, world: int) -> list[int]:
     return open_peer_shards(store, gathered, rank)
 
 
-def exchange_rows(ids, dest, world: int, serve):
+def exchange_rows(ids, dest, world: int, serve, counts=None):
     """Request/serve row exchange over torch.distributed (the NCCL transport of
     the group prefetch; any backend with all_to_all_single works, gloo on CPU
     in the tests).  The reference pulls rows per owner over TCP
@@ -110,20 +110,25 @@ def exchange_rows(ids, dest, world: int, serve):
     second one.
 
     ids  : 1-D int32 tensor of requested node ids (any order)
-    dest : owner rank of each id (same length)
+    dest : owner rank of each id (same length), or None when the caller
+           passes ids already grouped by owner rank with their `counts`
     serve: req_ids -> rows tensor [len(req_ids), stride] for ids this rank owns
     Returns (send_ids, rows): rows[i] is the row of send_ids[i] (ids regrouped
     by owner rank, stable)."""
     import torch
     import torch.distributed as dist
 
-    dest = dest.to(torch.int64)
-    order = torch.argsort(dest, stable=True)
-    send_ids = ids[order].contiguous()
-    counts = torch.bincount(dest, minlength=world).to(torch.int64)
-    recv_counts = torch.empty_like(counts)
-    dist.all_to_all_single(recv_counts, counts)
-    sc = [int(x) for x in counts.tolist()]
+    if counts is None:
+        dest = dest.to(torch.int64)
+        order = torch.argsort(dest, stable=True)
+        send_ids = ids[order].contiguous()
+        counts_t = torch.bincount(dest, minlength=world).to(torch.int64)
+    else:
+        send_ids = ids.contiguous()
+        counts_t = torch.tensor(counts, dtype=torch.int64, device=ids.device)
+    recv_counts = torch.empty_like(counts_t)
+    dist.all_to_all_single(recv_counts, counts_t)
+    sc = [int(x) for x in counts_t.tolist()]
     rc = [int(x) for x in recv_counts.tolist()]
     req = torch.empty(sum(rc), dtype=ids.dtype, device=ids.device)
     dist.all_to_all_single(req, send_ids, rc, sc)

@@ -100,6 +100,13 @@ class WorkerPipeline:
             self.owner_rank = (st.owner.to(torch.int64) % self.world).to(torch.uint8)
             self.nccl_peers = [q for q in range(st.k) if q % self.world != self.rank]
             st.peer_mask = sum(1 << q for q in self.nccl_peers)
+            # kinds (partitions) held by each rank: the per-owner request lists
+            # come out of one masked union + compaction per peer rank, already
+            # grouped by owner and sorted (no argsort)
+            self.rank_kinds = [sum(1 << q for q in range(st.k) if q % self.world == r)
+                               for r in range(self.world)]
+            self.pf_req = torch.empty((self.world, st.n), dtype=I32, device=dev)
+            self.pf_req_n = torch.zeros(self.world, dtype=I32, device=dev)
         peers = [q for q in range(st.k) if (st.peer_mask >> q) & 1]
         self.pf_peers = peers
         self.shadow = []
@@ -131,27 +138,42 @@ class WorkerPipeline:
         for q, t in self.shadow[slot].items():
             dst[q] = t.data_ptr()
         nid = ptr(self.pf_n) + 4 * slot
+        if self.pf_transport == "nccl":
+            self._exchange_nccl(ng, smp, slot, route, dst)
+            self.pf_rows += self.pf_n[slot]
+            self.launches += 6
+            return
         _lib.call("rg_route_kind_bits", ptr(route), st.n, st.peer_mask, ptr(self.pf_mask), s)
         _lib.call("rg_group_union", ptr(smp.bm), nw, ng, ptr(self.pf_mask), ptr(self.pf_union), s)
         _lib.call("rg_bitmap_compact", ptr(self.pf_union), nw, 1, ptr(self.pf_chunk),
                   ptr(self.pf_ids), st.n, nid, None, s)
-        if self.pf_transport == "nccl":
-            self._exchange_nccl(slot, route, dst)
-        else:
-            _lib.call("rg_prefetch_rows", ptr(self.pf_ids), nid, st.n, ptr(route),
-                      bases_array(st.bases), bases_array(dst),
-                      st.src_stride, st.stride, s)
+        _lib.call("rg_prefetch_rows", ptr(self.pf_ids), nid, st.n, ptr(route),
+                  bases_array(st.bases), bases_array(dst), st.src_stride, st.stride, s)
         self.pf_rows += self.pf_n[slot]
         self.launches += 6
 
-    def _exchange_nccl(self, slot: int, route, dst) -> None:
+    def _exchange_nccl(self, ng: int, smp, slot: int, route, dst) -> None:
         """NCCL transport: requested ids to their owners, rows back, scatter
-        into shadow[slot] (current stream; one host sync for the sizes)."""
-        st = self.store
-        n = int(self.pf_n[slot].item())
-        ids = self.pf_ids[:n]
-        dest = self.owner_rank[ids.long()]
-        send_ids, rows = multigpu.exchange_rows(ids, dest, self.world, self._serve)
+        into shadow[slot] (current stream; one host sync for the sizes).
+        The request list for owner rank r = compaction of the group union
+        masked with r's kinds, so the lists arrive grouped and sorted."""
+        st, s = self.store, _lib.stream_handle()
+        nw = self.dg.nwords
+        for r in range(self.world):
+            if r == self.rank:
+                continue
+            _lib.call("rg_route_kind_bits", ptr(route), st.n, self.rank_kinds[r],
+                      ptr(self.pf_mask), s)
+            _lib.call("rg_group_union", ptr(smp.bm), nw, ng, ptr(self.pf_mask),
+                      ptr(self.pf_union), s)
+            _lib.call("rg_bitmap_compact", ptr(self.pf_union), nw, 1, ptr(self.pf_chunk),
+                      ptr(self.pf_req[r]), st.n, ptr(self.pf_req_n) + 4 * r, None, s)
+        counts = self.pf_req_n.cpu().tolist()  # one host sync for every split size
+        counts[self.rank] = 0
+        self.pf_n[slot] = sum(counts)
+        ids = torch.cat([self.pf_req[r, :counts[r]] for r in range(self.world)])
+        send_ids, rows = multigpu.exchange_rows(ids, None, self.world, self._serve,
+                                                counts=counts)
         _lib.call("rg_scatter_rows", ptr(send_ids), send_ids.numel(), ptr(route), ptr(rows),
                   st.src_stride, bases_array(dst), st.src_stride, st.src_stride,
                   _lib.stream_handle())
