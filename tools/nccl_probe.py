@@ -1,4 +1,5 @@
-"""2-rank breakdown of the NCCL group-prefetch exchange (Products, G=64)."""
+"""Phase breakdown of the NCCL group-prefetch exchange (Products, G=64, no hot cache):
+torchrun --nproc-per-node 2 tools/nccl_probe.py"""
 import os, sys, time
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch, torch.distributed as dist
@@ -29,12 +30,16 @@ orig = multigpu.exchange_rows
 T = {}
 def ev():
     e = torch.cuda.Event(enable_timing=True); e.record(); return e
-def timed_exchange(ids_, dest, world_, serve):
+def timed_exchange(ids_, dest, world_, serve, counts=None):
     e0 = ev()
-    dest = dest.to(torch.int64)
-    order = torch.argsort(dest, stable=True)
-    send_ids = ids_[order].contiguous()
-    counts = torch.bincount(dest, minlength=world_).to(torch.int64)
+    if counts is None:
+        dest = dest.to(torch.int64)
+        order = torch.argsort(dest, stable=True)
+        send_ids = ids_[order].contiguous()
+        counts = torch.bincount(dest, minlength=world_).to(torch.int64)
+    else:  # already grouped by owner (pipeline: masked union per peer rank)
+        send_ids = ids_.contiguous()
+        counts = torch.tensor(counts, dtype=torch.int64, device=ids_.device)
     e1 = ev()
     recv_counts = torch.empty_like(counts)
     dist.all_to_all_single(recv_counts, counts)
