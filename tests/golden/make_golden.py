@@ -33,7 +33,7 @@ sys.path.insert(0, REF)
 from gnnpipe.cache import build_steady  # noqa: E402
 from gnnpipe.graph import from_edge_list, synth_powerlaw  # noqa: E402
 from gnnpipe.partition import partition_edgecut  # noqa: E402
-from gnnpipe.plan import FrequencyTable, collect_access, generate_plan, top_hot  # noqa: E402
+from gnnpipe.plan import collect_access, generate_plan, top_hot  # noqa: E402
 from gnnpipe.prefetch import assemble_bundle  # noqa: E402
 from gnnpipe.sampler import SeedSchedule, epoch_batches, sample_block  # noqa: E402
 from gnnpipe.store import InprocTransport, StoreClient, StoreShard, TransferAccount  # noqa: E402

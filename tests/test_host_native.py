@@ -68,7 +68,6 @@ def test_synth_powerlaw_matches_reference_hashes(golden, name):
 def test_full_size_generator_structure(golden, name):
     """Products-shape CSR + LDG owners equal the reference's at full size."""
     from paper_2505_10806_b200.graph import synth_powerlaw_csr
-    from paper_2505_10806_b200.partition import PartitionBook  # noqa: F401
     from paper_2505_10806_b200 import _lib
 
     rec = golden["generator"][name]

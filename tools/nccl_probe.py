@@ -3,7 +3,7 @@ torchrun --nproc-per-node 2 tools/nccl_probe.py"""
 import os, sys, time
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch, torch.distributed as dist
-from paper_2505_10806_b200 import multigpu, _lib
+from paper_2505_10806_b200 import multigpu
 from paper_2505_10806_b200.engine import DeviceGraph, FeatureStore
 from paper_2505_10806_b200.graph import synth_powerlaw
 from paper_2505_10806_b200.partition import partition_edgecut
