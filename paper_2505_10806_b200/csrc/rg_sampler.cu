@@ -28,7 +28,6 @@ constexpr int kSlowCap = 4096;            // largest take handled (fanout cap)
 constexpr int kCompactWords = 1024;       // bitmap words per compaction CTA
 constexpr int kCompactThreads = 256;
 constexpr int kScanElems = 1024;          // elements per ELL-scan CTA
-constexpr int kMaxGroupSeeds = 64;        // batches whose step seed is kept in smem
 constexpr int kFloydBits = 65536;         // PRNG slow path: largest degree with fanout > 32
 
 __device__ __forceinline__ void mark(uint32_t* bm, int32_t v) {
