@@ -90,9 +90,10 @@ int rg_mark_seeds(const int32_t* d_seeds, const int32_t* d_nseeds, int32_t G, in
  *   batch bitmap, so after the step bm = F_d U src (sampler.py:148).
  * d_slow: scratch of 1 + G*cap_in int32, required only when fanout > 32
  * (rows with take > 32 go to a CTA-per-row path); fanout <= 4096.
- * d_meta: optional scratch of G*cap_in x 16 B (int4 per slot); when given,
- * a lane-parallel pass first stores (row start, degree, id) of every
- * frontier node so the per-node warps skip the front -> indptr chain.
+ * d_meta: scratch of (G*cap_in + 1) x 16 B: a lane-parallel pass first
+ * stores (row start, degree, id) of every frontier node (int4 per slot) so
+ * the per-node warps skip the front -> indptr chain; the last record holds
+ * the launch-wide work-queue counter.
  * sorted_rows != 0 promises every CSR row is ascending (true for the
  * reference's generator and from_edge_list): selected positions are then
  * emitted in position order without a sort.                            */

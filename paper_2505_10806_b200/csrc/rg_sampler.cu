@@ -29,6 +29,8 @@ constexpr int kCompactWords = 1024;       // bitmap words per compaction CTA
 constexpr int kCompactThreads = 256;
 constexpr int kScanElems = 1024;          // elements per ELL-scan CTA
 constexpr int kFloydBits = 65536;         // PRNG slow path: largest degree with fanout > 32
+constexpr int kQueueBatches = 128;        // largest group G of one rg_sample_level call
+constexpr unsigned kClaim = 4;            // items a warp claims from the launch queue
 
 __device__ __forceinline__ void mark(uint32_t* bm, int32_t v) {
   atomicOr(bm + (v >> 5), 1u << (v & 31));
@@ -242,33 +244,48 @@ __global__ void __launch_bounds__(kSampleWarps * 32)
                         const int32_t* __restrict__ nfront, int F, uint64_t level_mix,
                         const uint64_t* __restrict__ rng_seed, int32_t* __restrict__ ell,
                         int32_t* __restrict__ cnt, uint32_t* __restrict__ bm, int64_t nwords,
-                        int32_t* __restrict__ slow, int sorted_rows, int prng) {
-  __shared__ int s_next;
+                        int32_t* __restrict__ slow, int sorted_rows, int prng,
+                        unsigned* __restrict__ queue) {
   __shared__ uint64_t s_key[kSampleWarps][64];
   __shared__ int32_t s_pos[kSampleWarps][96];
-  __shared__ uint64_t s_seed[1];  // this CTA's batch step seed s_d
+  __shared__ uint64_t s_seed[kQueueBatches];  // step seed s_d of every batch
+  __shared__ int32_t s_nf[kQueueBatches];     // frontier size of every batch
+  __shared__ unsigned s_items;
   const int lane = lane_id();
   const int warp = threadIdx.x >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
-  if (threadIdx.x == 0) {
-    s_seed[0] = mix64(rng_seed[blockIdx.y] ^ level_mix);
-    s_next = 0;
-  }
+  if (threadIdx.x == 0) s_items = 0;
   __syncthreads();
-  // batch b = blockIdx.y; its CTAs c = blockIdx.x own frontier ranks
-  // j = c, c + gridDim.x, ... (the low, hub-heavy ranks spread over all of
-  // them) and their warps pull those ranks through a shared counter.
-  const int b = blockIdx.y;
-  const int nfb = nfront[b];
-  const unsigned gx = gridDim.x;
+  int mx = 0;
+  for (int i = threadIdx.x; i < G; i += blockDim.x) {
+    const int nf = nfront[i];
+    if (i < kQueueBatches) {
+      s_seed[i] = mix64(rng_seed[i] ^ level_mix);
+      s_nf[i] = nf;
+    }
+    mx = max(mx, nf);
+  }
+  atomicMax(&s_items, (unsigned)mx);
+  __syncthreads();
+  // one launch-wide queue of items k = j*G + b (frontier rank j of batch b):
+  // rank-major, so the low (hub-heavy) ranks of every batch go first and the
+  // light tail balances across all SMs; warps claim kClaim items at a time
+  const unsigned items = s_items * (unsigned)G;
+  // batches past the shared-memory tables (G > kQueueBatches: API callers
+  // sampling thousands of seeds sets at once) read / derive theirs
+  auto step_seed = [&](int b) {
+    return b < kQueueBatches ? s_seed[b] : mix64(__ldg(rng_seed + b) ^ level_mix);
+  };
   for (;;) {
-    int t = 0;
-    if (lane == 0) t = atomicAdd(&s_next, 1);
-    t = __shfl_sync(kFull, t, 0);
-    const unsigned ju = blockIdx.x + (unsigned)t * gx;
-    if (ju >= (unsigned)nfb) break;
-    const int j = (int)ju;
-    const unsigned k = (unsigned)j * (unsigned)G + (unsigned)b;  // item id (slow path)
+    unsigned t0 = 0;
+    if (lane == 0) t0 = atomicAdd(queue, (unsigned)kClaim);
+    t0 = __shfl_sync(kFull, t0, 0);
+    if (t0 >= items) break;
+#pragma unroll 1
+  for (unsigned k = t0; k < t0 + kClaim && k < items; ++k) {
+    const int j = (int)(k / (unsigned)G);
+    const int b = (int)(k - (unsigned)j * (unsigned)G);
+    if (j >= (b < kQueueBatches ? s_nf[b] : __ldg(nfront + b))) continue;
     const int64_t row = (int64_t)b * cap_in + j;
     int32_t v;
     int64_t a;
@@ -295,7 +312,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32)
     int32_t* out = ell + row * F;
     uint32_t* bmb = bm + (int64_t)b * nwords;
     if (kVariants && D > F) {
-      const uint64_t sd = s_seed[0];
+      const uint64_t sd = step_seed(b);
       const uint64_t nk = mix64(((uint64_t)v + 1ull) * GOLDEN ^ sd);
       int p = prng_positions(prng, nk, sd, D, T);
       int32_t x = INT_MAX;
@@ -322,7 +339,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32)
       if (D <= F) {
         sel = D == 32 ? kFull : ((1u << D) - 1u);
       } else {
-        const uint64_t sd = s_seed[0];
+        const uint64_t sd = step_seed(b);
         const uint64_t nk = mix64(((uint64_t)v + 1ull) * GOLDEN ^ sd);
         const uint64_t key = lane < D ? mix64(nk + (uint64_t)(lane + 1) * GOLDEN) : ~0ull;
         sel = select_mask32(key, __ballot_sync(kFull, lane < D), T);
@@ -345,7 +362,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32)
       continue;
     }
     // D > 32 (> F): threshold candidates, else the running top-T list
-    const uint64_t sd = s_seed[0];
+    const uint64_t sd = step_seed(b);
     const uint64_t nk = mix64(((uint64_t)v + 1ull) * GOLDEN ^ sd);
     int pos;
     const bool ordered = select_threshold(nk, D, F, s_key[warp], s_pos[warp], pos);  // T == F here
@@ -367,7 +384,8 @@ __global__ void __launch_bounds__(kSampleWarps * 32)
       out[lane] = nb;
       mark(bmb, nb);
     }
-  }
+  }  // items of the claim
+  }  // claims
 }
 
 // ---- take > 32 (fanout > 32): one CTA per node, shared-memory sort -------
@@ -713,25 +731,30 @@ extern "C" int rg_sample_level(const int64_t* d_indptr, const int32_t* d_indices
   int32_t* slow = fanout > 32 ? d_slow : nullptr;
   if (slow && cudaMemsetAsync(slow, 0, sizeof(int32_t), s) != cudaSuccess)
     return check_launch("sample_level memset");
+  RG_REQUIRE(d_meta != nullptr, "rg_sample_level: d_meta scratch is required");
+  RG_REQUIRE((uint64_t)G * (uint64_t)cap_in < (1ull << 32) - kClaim,
+             "rg_sample_level: G * cap_in above the 32-bit work queue");
   int4* meta = reinterpret_cast<int4*>(d_meta);
-  if (meta) {
+  // launch-wide work queue: the extra record after the G*cap_in meta records
+  unsigned* queue = reinterpret_cast<unsigned*>(meta + (int64_t)G * cap_in);
+  if (cudaMemsetAsync(queue, 0, sizeof(unsigned), s) != cudaSuccess)
+    return check_launch("sample_level queue");
+  {
     const int bx = (int)std::min<int64_t>((cap_in + 255) / 256, std::max(1, kNumSMs * 16 / G));
     node_meta_kernel<<<dim3(bx, G), 256, 0, s>>>(d_indptr, d_front, cap_in, d_nfront, meta);
     if (int rc = check_launch("node_meta")) return rc;
   }
-  const int grid = kNumSMs * 5;  // 48 regs x 256 threads: 5 CTAs per SM
+  // one wave: 48 regs x 256 threads = 5 CTAs per SM (4 for the PRNG variants);
   // SplitMix64 keys (the reference) and the PRNG variants are separate
   // instantiations so the reference path keeps its register budget
   if (prng == kSplitMix)
-    sample_level_kernel<false><<<dim3(std::max(1, grid / G), G), kSampleWarps * 32, 0,
-                                 s>>>(d_indptr, d_indices, G, d_front, meta, cap_in, d_nfront, fanout,
-                                      level_mix, d_rng_seed, d_ell, d_cnt, d_bm, nwords, slow,
-                                      sorted_rows, prng);
+    sample_level_kernel<false><<<kNumSMs * 5, kSampleWarps * 32, 0, s>>>(
+        d_indptr, d_indices, G, d_front, meta, cap_in, d_nfront, fanout, level_mix, d_rng_seed,
+        d_ell, d_cnt, d_bm, nwords, slow, sorted_rows, prng, queue);
   else
-    sample_level_kernel<true><<<dim3(std::max(1, kNumSMs * 4 / G), G),
-                                kSampleWarps * 32, 0, s>>>(
-        d_indptr, d_indices, G, d_front, meta, cap_in, d_nfront, fanout, level_mix, d_rng_seed, d_ell,
-        d_cnt, d_bm, nwords, slow, sorted_rows, prng);
+    sample_level_kernel<true><<<kNumSMs * 4, kSampleWarps * 32, 0, s>>>(
+        d_indptr, d_indices, G, d_front, meta, cap_in, d_nfront, fanout, level_mix, d_rng_seed,
+        d_ell, d_cnt, d_bm, nwords, slow, sorted_rows, prng, queue);
   int rc = check_launch("sample_level");
   if (rc || !slow) return rc;
   sample_slow_kernel<<<kNumSMs, 256, 0, s>>>(d_indptr, d_indices, G, d_front, cap_in, fanout,

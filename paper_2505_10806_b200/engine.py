@@ -135,7 +135,8 @@ class BlockSampler:
         self.slow = (torch.empty(1 + G * max(caps[:-1]), dtype=I32, device=dev)
                      if max(self.step_fan) > 32 else None)
         # per-slot (row start, degree, id) records for the sampler (16 B each)
-        self.meta = torch.empty((G, max(caps[:-1]), 4), dtype=I32, device=dev)
+        # (+1 record: the sampler's launch-wide work-queue counter)
+        self.meta = torch.empty((G * max(caps[:-1]) + 1, 4), dtype=I32, device=dev)
 
     def set_seeds(self, b: int, seeds: np.ndarray, rng_seed: int) -> None:
         """Host seeds for slot b (API path; the plan path fills on device)."""
