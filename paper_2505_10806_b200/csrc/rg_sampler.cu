@@ -16,6 +16,7 @@
 // over all n nodes that accumulates across steps; rg_bitmap_compact turns it
 // into the sorted-unique id list.
 #include <climits>
+#include <cstdlib>
 
 #include "rg_common.cuh"
 #include "rg_prng.cuh"
@@ -30,7 +31,9 @@ constexpr int kCompactThreads = 256;
 constexpr int kScanElems = 1024;          // elements per ELL-scan CTA
 constexpr int kFloydBits = 65536;         // PRNG slow path: largest degree with fanout > 32
 constexpr int kQueueBatches = 128;        // largest group G of one rg_sample_level call
-constexpr unsigned kClaim = 4;            // items a warp claims from the launch queue
+// items a warp claims from the launch queue per atomic (Products, batches/s:
+// 1 7,139; 2 8,267; 4 8,713; 8 8,843; 16 8,702)
+constexpr unsigned kClaim = 8;
 
 __device__ __forceinline__ void mark(uint32_t* bm, int32_t v) {
   atomicOr(bm + (v >> 5), 1u << (v & 31));
@@ -245,7 +248,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32)
                         const uint64_t* __restrict__ rng_seed, int32_t* __restrict__ ell,
                         int32_t* __restrict__ cnt, uint32_t* __restrict__ bm, int64_t nwords,
                         int32_t* __restrict__ slow, int sorted_rows, int prng,
-                        unsigned* __restrict__ queue) {
+                        unsigned* __restrict__ queue, unsigned claim) {
   __shared__ uint64_t s_key[kSampleWarps][64];
   __shared__ int32_t s_pos[kSampleWarps][96];
   __shared__ uint64_t s_seed[kQueueBatches];  // step seed s_d of every batch
@@ -278,11 +281,11 @@ __global__ void __launch_bounds__(kSampleWarps * 32)
   };
   for (;;) {
     unsigned t0 = 0;
-    if (lane == 0) t0 = atomicAdd(queue, (unsigned)kClaim);
+    if (lane == 0) t0 = atomicAdd(queue, claim);
     t0 = __shfl_sync(kFull, t0, 0);
     if (t0 >= items) break;
 #pragma unroll 1
-  for (unsigned k = t0; k < t0 + kClaim && k < items; ++k) {
+  for (unsigned k = t0; k < t0 + claim && k < items; ++k) {
     const int j = (int)(k / (unsigned)G);
     const int b = (int)(k - (unsigned)j * (unsigned)G);
     if (j >= (b < kQueueBatches ? s_nf[b] : __ldg(nfront + b))) continue;
@@ -744,17 +747,22 @@ extern "C" int rg_sample_level(const int64_t* d_indptr, const int32_t* d_indices
     node_meta_kernel<<<dim3(bx, G), 256, 0, s>>>(d_indptr, d_front, cap_in, d_nfront, meta);
     if (int rc = check_launch("node_meta")) return rc;
   }
-  // one wave: 48 regs x 256 threads = 5 CTAs per SM (4 for the PRNG variants);
+  static const unsigned claim = [] {
+    const char* e = getenv("RG_SAMPLER_CLAIM");
+    return e ? (unsigned)std::max(1, atoi(e)) : kClaim;
+  }();
+  // one wave: 48 regs x 256 threads = 5 CTAs per SM (4 for the PRNG variants;
+  // capping at 40 regs for 6/SM measured 1-2 % slower);
   // SplitMix64 keys (the reference) and the PRNG variants are separate
   // instantiations so the reference path keeps its register budget
   if (prng == kSplitMix)
     sample_level_kernel<false><<<kNumSMs * 5, kSampleWarps * 32, 0, s>>>(
         d_indptr, d_indices, G, d_front, meta, cap_in, d_nfront, fanout, level_mix, d_rng_seed,
-        d_ell, d_cnt, d_bm, nwords, slow, sorted_rows, prng, queue);
+        d_ell, d_cnt, d_bm, nwords, slow, sorted_rows, prng, queue, claim);
   else
     sample_level_kernel<true><<<kNumSMs * 4, kSampleWarps * 32, 0, s>>>(
         d_indptr, d_indices, G, d_front, meta, cap_in, d_nfront, fanout, level_mix, d_rng_seed,
-        d_ell, d_cnt, d_bm, nwords, slow, sorted_rows, prng, queue);
+        d_ell, d_cnt, d_bm, nwords, slow, sorted_rows, prng, queue, claim);
   int rc = check_launch("sample_level");
   if (rc || !slow) return rc;
   sample_slow_kernel<<<kNumSMs, 256, 0, s>>>(d_indptr, d_indices, G, d_front, cap_in, fanout,
