@@ -11,6 +11,7 @@
 // 32 lanes busy (flattened row x vector index) and written back contiguously.
 // Source rows may live in this GPU's HBM or in a peer GPU's shard (NVLink
 // P2P pointer); the kernel does not distinguish.
+#include <atomic>
 #include <cstdlib>
 
 #include "rg_common.cuh"
@@ -153,6 +154,145 @@ __global__ void __launch_bounds__(kGatherWarps * 32, 4)
         atomicAdd(g, x);
     }
   }
+}
+
+// ---- launch-wide work queue (local rows) -----------------------------------
+// Same copy as the flattened path above, but 32-row chunks are pulled from a
+// launch-wide queue instead of each CTA striding over one batch: items
+// k = c*G + b (chunk c of batch b) chunk-major, so the work in flight at any
+// time spans every batch at the same chunk index (hub rows, low ids, are
+// shared across batches and stay in L2) and the tail balances across SMs.
+// Provenance counters accumulate per CTA per batch in shared memory.
+constexpr int kQueueMaxG = 128;  // batches with shared-memory counters
+constexpr unsigned kGatherClaim = 4;
+
+__global__ void __launch_bounds__(kGatherWarps * 32, 4)
+    gather_queue_kernel(const int32_t* __restrict__ ids, const int32_t* __restrict__ nids,
+                        int64_t cap, int G, const uint32_t* __restrict__ route,
+                        const __grid_constant__ Bases bases, int src_stride, int stride,
+                        int nvec, int dq, int dr, int my_part, float* __restrict__ out,
+                        uint32_t* __restrict__ counters, unsigned* __restrict__ queue) {
+  __shared__ uint32_t s_cnt[kQueueMaxG][RG_NCOUNTERS];
+  __shared__ int32_t s_nr[kQueueMaxG];
+  __shared__ const float* s_base[16];
+  __shared__ unsigned s_maxc;
+  const int lane = lane_id();
+  for (int i = threadIdx.x; i < kQueueMaxG * RG_NCOUNTERS; i += blockDim.x)
+    (&s_cnt[0][0])[i] = 0;
+  if (threadIdx.x < 16) s_base[threadIdx.x] = bases.p[threadIdx.x];
+  if (threadIdx.x == 0) s_maxc = 0;
+  __syncthreads();
+  unsigned mc = 0;
+  for (int i = threadIdx.x; i < G; i += blockDim.x) {
+    const int n = nids[i];
+    s_nr[i] = n;
+    mc = max(mc, (unsigned)((n + 31) / 32));
+  }
+  atomicMax(&s_maxc, mc);
+  __syncthreads();
+  const unsigned items = s_maxc * (unsigned)G;
+  for (;;) {
+    unsigned t0 = 0;
+    if (lane == 0) t0 = atomicAdd(queue, kGatherClaim);
+    t0 = __shfl_sync(kFull, t0, 0);
+    if (t0 >= items) break;
+#pragma unroll 1
+    for (unsigned k = t0; k < t0 + kGatherClaim && k < items; ++k) {
+      const int c = (int)(k / (unsigned)G);
+      const int b = (int)(k - (unsigned)c * (unsigned)G);
+      const int nrows = s_nr[b];
+      const int64_t r0 = (int64_t)c * 32;
+      if (r0 >= nrows) continue;
+      const int64_t row = r0 + lane;
+      const bool valid = row < nrows;
+      const int nr = (int)(nrows - r0 < 32 ? nrows - r0 : 32);
+      uint32_t rt = RG_ROUTE_INVALID;
+      if (valid) rt = __ldg(route + __ldg(ids + (int64_t)b * cap + row));
+      const int kind = (int)(rt >> RG_KIND_SHIFT);
+      const float* bp = (valid && rt != RG_ROUTE_INVALID) ? s_base[kind] : nullptr;
+      const bool bad = valid && bp == nullptr;
+      const bool local = valid && !bad && kind == my_part;
+      const bool hit = valid && !bad && kind == (int)RG_KIND_CACHE;
+      const bool fb = valid && !bad && !local && !hit;
+      const unsigned n_local = __popc(__ballot_sync(kFull, local));
+      const unsigned n_hit = __popc(__ballot_sync(kFull, hit));
+      const unsigned n_fb = __popc(__ballot_sync(kFull, fb));
+      const unsigned n_bad = __popc(__ballot_sync(kFull, bad));
+      const unsigned om = __reduce_or_sync(kFull, fb ? (1u << kind) : 0u);
+      if (lane == 0) {
+        uint32_t* sc = s_cnt[b];
+        if (n_local) atomicAdd(sc + RG_CNT_LOCAL, n_local);
+        if (n_hit) atomicAdd(sc + RG_CNT_HIT, n_hit);
+        if (n_fb) atomicAdd(sc + RG_CNT_FALLBACK, n_fb);
+        if (n_bad) atomicAdd(sc + RG_CNT_BAD, n_bad);
+        if (om) atomicOr(sc + RG_CNT_OWNER_MASK, om);
+      }
+      const float* src = nullptr;
+      if (bp) src = bp + (int64_t)(rt & RG_ROW_MASK) * src_stride;
+      const unsigned long long srcu = reinterpret_cast<unsigned long long>(src);
+      float4* dst = reinterpret_cast<float4*>(out + ((int64_t)b * cap + r0) * stride);
+      const int total = nr * nvec;
+      int er = lane / nvec, ec = lane - (lane / nvec) * nvec;
+      for (int e0 = 0; e0 < total; e0 += 32 * kUnroll) {
+        float4 v[kUnroll];
+        int rr[kUnroll], cc[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          rr[u] = er;
+          cc[u] = ec;
+          ec += dr;
+          er += dq;
+          if (ec >= nvec) {
+            ec -= nvec;
+            ++er;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          const unsigned long long sp = __shfl_sync(kFull, srcu, rr[u] & 31);
+          const int e = e0 + u * 32 + lane;
+          if (e < total && sp)
+            v[u] = ld_stream(reinterpret_cast<const float4*>(sp) + cc[u]);
+          else
+            v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          const int e = e0 + u * 32 + lane;
+          if (e < total) st_stream(dst + e, v[u]);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < G * RG_NCOUNTERS; i += blockDim.x) {
+    const int b = i / RG_NCOUNTERS, k = i - b * RG_NCOUNTERS;
+    const uint32_t x = s_cnt[b][k];
+    if (x) {
+      uint32_t* g = counters + (int64_t)b * RG_NCOUNTERS + k;
+      if (k == RG_CNT_OWNER_MASK)
+        atomicOr(g, x);
+      else
+        atomicAdd(g, x);
+    }
+  }
+}
+
+// per-device ring of queue counters: one slot per launch (zeroed on the
+// launch stream), so concurrent gathers on different streams never share
+unsigned* queue_slot(cudaStream_t s) {
+  constexpr int kSlots = 1024;
+  static unsigned* ring[16] = {};
+  static std::atomic<unsigned> next{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return nullptr;
+  if (!ring[dev] && cudaMalloc(&ring[dev], kSlots * sizeof(unsigned)) != cudaSuccess) {
+    ring[dev] = nullptr;
+    return nullptr;
+  }
+  unsigned* q = ring[dev] + (next.fetch_add(1) % kSlots);
+  if (cudaMemsetAsync(q, 0, sizeof(unsigned), s) != cudaSuccess) return nullptr;
+  return q;
 }
 
 // ---- staged peer rows (multi-GPU) ---------------------------------------
@@ -403,6 +543,19 @@ extern "C" int rg_gather_bundle(const int32_t* d_ids, const int32_t* d_nids, int
   const int64_t want = (cap + kGatherWarps * 32 - 1) / (kGatherWarps * 32);
   const int gx = (int)std::max<int64_t>(
       1, std::min<int64_t>(want, ((int64_t)kNumSMs * ctas_per_sm) / G));
+  static const bool use_queue = [] {
+    const char* e = getenv("RG_GATHER_QUEUE");
+    return e ? atoi(e) != 0 : true;
+  }();
+  if (peer_mask == 0 && G <= kQueueMaxG && use_queue &&
+      (uint64_t)G * (uint64_t)((cap + 31) / 32) < (1ull << 32) - kGatherClaim) {
+    unsigned* q = queue_slot((cudaStream_t)stream);
+    if (!q) return check_launch("gather queue");
+    gather_queue_kernel<<<kNumSMs * ctas_per_sm, kGatherWarps * 32, 0, (cudaStream_t)stream>>>(
+        d_ids, d_nids, cap, G, d_route, bases, src_stride, stride, nvec, dq, dr, my_part, d_out,
+        d_counters, q);
+    return check_launch("gather_queue");
+  }
   if (peer_mask != 0)
     gather_bundle_kernel<true><<<dim3(gx, G), kGatherWarps * 32, 0, (cudaStream_t)stream>>>(
         d_ids, d_nids, cap, d_route, bases, src_stride, stride, nvec, dq, dr, my_part, peer_mask,
