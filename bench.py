@@ -34,11 +34,13 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "sample+fetch mini-batches/s, Products-shape, 1-8 B200; remote rows/epoch"
 CONFIGS = {
-    # group 64: at N > 1 a group's peer rows are prefetched once (their union
-    # is near the whole peer shard already at 32 batches), so the NVLink cost
-    # per batch halves from 32 to 64; N = 1 is indifferent (8,220 vs 8,219)
+    # group 128: the chunk-major gather queue serves rows shared by the group's
+    # batches from L2, so larger groups read less HBM (N = 1: G 32 / 64 / 96 /
+    # 128 -> 9,490 / 11,133 / 11,715 / 11,877 batches/s); at N > 1 a group's
+    # peer rows are prefetched once, so the NVLink cost per batch falls with G
+    # too.  ~130 GB of HBM per GPU (two 55 GB bundle slots).
     "products": dict(n=2_449_029, m=13, d=100, classes=47, fanouts=[15, 10, 5], batch=1024,
-                     parts=8, group=64),
+                     parts=8, group=128),
     "reddit": dict(n=232_965, m=246, d=602, classes=41, fanouts=[25, 10], batch=1024, parts=8),
     "c1": dict(n=100_000, m=10, d=128, classes=8, fanouts=[10, 5], batch=1024, parts=2),
     # config X: structure / masks / partition from the bit-exact native
@@ -363,7 +365,8 @@ def main():
         raise SystemExit("--transport nccl needs the group prefetch (no --pull / --staged)")
     store.build_route(shard_ids)
     train = np.flatnonzero(g.train_mask)
-    group = args.group or cfg.get("group", 32)
+    # --staged keeps a second full set of bundle-sized staging buffers: 32
+    group = args.group or (32 if args.staged else cfg.get("group", 32))
     pipe = WorkerPipeline(dg, store, part, train, cfg["fanouts"], cfg["batch"], S0, group,
                           nbuf=1 if (args.serial or args.graphs) else 2, prng=args.prng)
     nb, G = pipe.nb, pipe.G
@@ -573,7 +576,7 @@ def main():
                           "inputs larger than L2 (feature shards %.0f MB; bundle %.0f MB/batch)")
                          % ((feat_bytes / 1e6,) if flush
                             else (feat_bytes / 1e6, float(rows_b.mean()) * d * 4 / 1e6))},
-        "roofline": {"kernel": "gather_bundle_kernel", "bound": "hbm", "achieved": achieved,
+        "roofline": {"kernel": "gather_queue_kernel (rg_gather_bundle)", "bound": "hbm", "achieved": achieved,
                      "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic_b,
                      "bytes_per_launch": gather_bytes / args.steps,
@@ -672,9 +675,10 @@ def run_check(pipe, g, cfg, s0, prng="splitmix"):
 
 def run_e2e_host_rows(pipe, cfg, args, world):
     """Informational: the numpy-facing drop-in returns bundle rows on the
-    host, so each group's rows (the valid |input| x d part of every slot)
-    are copied to pinned host memory on a copy stream, overlapped with the
-    next group's sampling + gather.  PCIe-bound; bytes counted exactly."""
+    host, so every batch's rows (the valid |input| x d part of its slot) are
+    copied to pinned host memory on a copy stream, through a ring of two
+    batch-sized host buffers (a slot is reused once the host has seen the
+    copy that filled it).  PCIe-bound; bytes counted exactly."""
     import torch
     import torch.distributed as dist
 
@@ -682,29 +686,30 @@ def run_e2e_host_rows(pipe, cfg, args, world):
     d = cfg["d"]
     n_full = max(1, nb // G)
     steps = max(2, min(args.steps, 6))
-    host = [torch.empty((G, pipe.cap_in, d), dtype=torch.float32).pin_memory()
-            for _ in range(2)]
+    host = [torch.empty((pipe.cap_in, d), dtype=torch.float32).pin_memory() for _ in range(2)]
     copy = torch.cuda.Stream()
     done = [torch.cuda.Event(), torch.cuda.Event()]
     ready = torch.cuda.Event()
-    nbytes = 0
+    nbytes, q = 0, 0
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     t = time.perf_counter()
     for kk in range(steps):
         i0 = (kk % n_full) * G
-        done[kk % 2].synchronize()  # host buffer free again
         pipe.step(i0)
         nf = smp.nfront[smp.L, :G].cpu().numpy()
         ready.record()
-        with torch.cuda.stream(copy):
-            copy.wait_event(ready)
-            for b in range(G):
-                n = int(nf[b])
-                host[kk % 2][b, :n].copy_(pipe.rows[b, :n, :d], non_blocking=True)
-                nbytes += n * d * 4
-            done[kk % 2].record(copy)
+        for b in range(G):
+            slot = q % 2
+            q += 1
+            done[slot].synchronize()  # the host has the previous contents
+            n = int(nf[b])
+            with torch.cuda.stream(copy):
+                copy.wait_event(ready)
+                host[slot][:n].copy_(pipe.rows[b, :n, :d], non_blocking=True)
+                done[slot].record(copy)
+            nbytes += n * d * 4
         torch.cuda.current_stream().wait_stream(copy)  # rows buffer reused next step
     torch.cuda.synchronize()
     wall = time.perf_counter() - t
@@ -713,7 +718,8 @@ def run_e2e_host_rows(pipe, cfg, args, world):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     return {"value": steps * G * world / float(tt.item()), "unit": "batches/s",
             "d2h_bytes_per_step": nbytes / steps, "steps": steps,
-            "api": "bundle rows to pinned host memory every step (numpy drop-in layout)"}
+            "api": "bundle rows to pinned host memory every step (numpy drop-in layout), "
+                   "2-batch pinned ring"}
 
 
 def run_e2e(pipe, g, cfg, args, world, staged=False):

@@ -654,7 +654,8 @@ def test_two_gpu_peer_gather_bit_exact(mode):
     s.close()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(port), str(root / "bench.py"),
-           "--gpus", "2", "--steps", "2", "--warmup", "1", "--no-cpu", "--no-e2e", "--check"]
+           "--gpus", "2", "--steps", "2", "--warmup", "1", "--no-cpu", "--no-e2e", "--check",
+           "--group", "32"]  # correctness run: small groups (staged doubles the bundle memory)
     if mode == "pull":
         cmd.append("--pull")
     elif mode == "nccl":
