@@ -84,12 +84,46 @@ __device__ __forceinline__ int select_positions(uint64_t nk, int D, int T) {
 // Distinct keys make it terminate after ~log2(32) informative bits.
 __device__ __forceinline__ unsigned select_mask32(uint64_t key, unsigned cand, int need,
                                                   int top_bit = 63) {
+  // two key bits per iteration: the candidates split into four buckets
+  // (00, 01, 10, 11) by two ballots; whole buckets below the cut are taken,
+  // the bucket holding the cut stays the candidate set.  All quantities are
+  // warp-uniform, so the branches do not diverge.
   unsigned sel = 0;
-  const uint32_t hi = (uint32_t)(key >> 32), lo = (uint32_t)key;
+  int bit = top_bit;
 #pragma unroll 1
-  for (int bit = top_bit; bit >= 0; --bit) {
-    const uint32_t w = bit >= 32 ? hi : lo;
-    const unsigned ones = __ballot_sync(kFull, (w >> (bit & 31)) & 1u);
+  for (; bit >= 1; bit -= 2) {
+    const uint32_t two = (uint32_t)(key >> (bit - 1)) & 3u;
+    const unsigned b1 = __ballot_sync(kFull, two & 2u);
+    const unsigned b0 = __ballot_sync(kFull, two & 1u);
+    const unsigned m0 = cand & ~b1 & ~b0;
+    const int n0 = __popc(m0);
+    if (n0 >= need) {
+      cand = m0;
+    } else {
+      sel |= m0;
+      need -= n0;
+      const unsigned m1 = cand & ~b1 & b0;
+      const int n1 = __popc(m1);
+      if (n1 >= need) {
+        cand = m1;
+      } else {
+        sel |= m1;
+        need -= n1;
+        const unsigned m2 = cand & b1 & ~b0;
+        const int n2 = __popc(m2);
+        if (n2 >= need) {
+          cand = m2;
+        } else {
+          sel |= m2;
+          need -= n2;
+          cand &= b1 & b0;
+        }
+      }
+    }
+    if (__popc(cand) == need) return sel | cand;
+  }
+  if (bit == 0) {  // odd number of bits: the last one alone
+    const unsigned ones = __ballot_sync(kFull, (uint32_t)key & 1u);
     const unsigned zeros = cand & ~ones;
     const int nz = __popc(zeros);
     if (nz >= need) {
