@@ -138,16 +138,64 @@ __device__ __forceinline__ unsigned select_mask32(uint64_t key, unsigned cand, i
   return sel;
 }
 
-// Same over up to 64 keys, two per lane (k0: candidate lane, k1: 32+lane).
+// Same over up to 64 keys, two per lane (k0: candidate lane, k1: 32+lane),
+// two key bits per iteration.
 __device__ __forceinline__ void select_mask64(uint64_t k0, uint64_t k1, unsigned c0, unsigned c1,
                                               int need, unsigned& s0, unsigned& s1,
                                               int top_bit = 63) {
   s0 = 0;
   s1 = 0;
+  int bit = top_bit;
 #pragma unroll 1
-  for (int bit = top_bit; bit >= 0; --bit) {
-    const unsigned o0 = __ballot_sync(kFull, (k0 >> bit) & 1ull);
-    const unsigned o1 = __ballot_sync(kFull, (k1 >> bit) & 1ull);
+  for (; bit >= 1; bit -= 2) {
+    const uint32_t t0 = (uint32_t)(k0 >> (bit - 1)) & 3u;
+    const uint32_t t1 = (uint32_t)(k1 >> (bit - 1)) & 3u;
+    const unsigned a1 = __ballot_sync(kFull, t0 & 2u), a0 = __ballot_sync(kFull, t0 & 1u);
+    const unsigned b1 = __ballot_sync(kFull, t1 & 2u), b0 = __ballot_sync(kFull, t1 & 1u);
+    // buckets in key order: (~x1 & ~x0), (~x1 & x0), (x1 & ~x0), (x1 & x0)
+    unsigned q0 = c0 & ~a1 & ~a0, q1 = c1 & ~b1 & ~b0;
+    int n = __popc(q0) + __popc(q1);
+    if (n >= need) {
+      c0 = q0;
+      c1 = q1;
+    } else {
+      s0 |= q0;
+      s1 |= q1;
+      need -= n;
+      q0 = c0 & ~a1 & a0;
+      q1 = c1 & ~b1 & b0;
+      n = __popc(q0) + __popc(q1);
+      if (n >= need) {
+        c0 = q0;
+        c1 = q1;
+      } else {
+        s0 |= q0;
+        s1 |= q1;
+        need -= n;
+        q0 = c0 & a1 & ~a0;
+        q1 = c1 & b1 & ~b0;
+        n = __popc(q0) + __popc(q1);
+        if (n >= need) {
+          c0 = q0;
+          c1 = q1;
+        } else {
+          s0 |= q0;
+          s1 |= q1;
+          need -= n;
+          c0 &= a1 & a0;
+          c1 &= b1 & b0;
+        }
+      }
+    }
+    if (__popc(c0) + __popc(c1) == need) {
+      s0 |= c0;
+      s1 |= c1;
+      return;
+    }
+  }
+  if (bit == 0) {
+    const unsigned o0 = __ballot_sync(kFull, (uint32_t)k0 & 1u);
+    const unsigned o1 = __ballot_sync(kFull, (uint32_t)k1 & 1u);
     const unsigned z0 = c0 & ~o0, z1 = c1 & ~o1;
     const int nz = __popc(z0) + __popc(z1);
     if (nz >= need) {
@@ -163,7 +211,6 @@ __device__ __forceinline__ void select_mask64(uint64_t k0, uint64_t k1, unsigned
     if (__popc(c0) + __popc(c1) == need) {
       s0 |= c0;
       s1 |= c1;
-      return;
     }
   }
 }
