@@ -196,10 +196,14 @@ __global__ void __launch_bounds__(kGatherWarps * 32, 4)
     if (lane == 0) t0 = atomicAdd(queue, kGatherClaim);
     t0 = __shfl_sync(kFull, t0, 0);
     if (t0 >= items) break;
+    int c = (int)(t0 / (unsigned)G);  // one division per claim
+    int b = (int)(t0 - (unsigned)c * (unsigned)G) - 1;
 #pragma unroll 1
     for (unsigned k = t0; k < t0 + kGatherClaim && k < items; ++k) {
-      const int c = (int)(k / (unsigned)G);
-      const int b = (int)(k - (unsigned)c * (unsigned)G);
+      if (++b == G) {
+        b = 0;
+        ++c;
+      }
       const int nrows = s_nr[b];
       const int64_t r0 = (int64_t)c * 32;
       if (r0 >= nrows) continue;

@@ -365,10 +365,15 @@ __global__ void __launch_bounds__(kSampleWarps * 32)
     if (lane == 0) t0 = atomicAdd(queue, claim);
     t0 = __shfl_sync(kFull, t0, 0);
     if (t0 >= items) break;
+  // one division per claim; consecutive items step (j, b) with a wrap
+  int j = (int)(t0 / (unsigned)G);
+  int b = (int)(t0 - (unsigned)j * (unsigned)G) - 1;
 #pragma unroll 1
   for (unsigned k = t0; k < t0 + claim && k < items; ++k) {
-    const int j = (int)(k / (unsigned)G);
-    const int b = (int)(k - (unsigned)j * (unsigned)G);
+    if (++b == G) {
+      b = 0;
+      ++j;
+    }
     if (j >= (b < kQueueBatches ? s_nf[b] : __ldg(nfront + b))) continue;
     const int64_t row = (int64_t)b * cap_in + j;
     int32_t v;
