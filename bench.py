@@ -607,9 +607,12 @@ def main():
                     "achieved_gbs": prefetch_rows * 4 * d / (prefetch_ms / 1e3) / 1e9,
                     "prefetch_ms_per_step": prefetch_ms / args.steps,
                     "peer_copy_ref_gbs": 770.0,
-                    "note": "peer-shard payload bytes copied over NVLink by the group "
-                            "prefetch, timed alone; 770 GB/s = measured peer copy per "
-                            "direction (B200_PROFILING.md)"}
+                    "note": ("peer-shard payload bytes copied over NVLink by the group "
+                             "prefetch, timed alone; 770 GB/s = measured peer copy per "
+                             "direction (B200_PROFILING.md)" if args.transport == "p2p" else
+                             "NCCL transport: the prefetch time also contains waits for the "
+                             "other ranks' matching collectives (ranks drift in the serial "
+                             "re-timing loop), so achieved_gbs understates the link")}
                    if world > 1 and pipe.prefetch and not staged else
                    {"mode": "staged" if staged else "per-batch pull",
                     "peer_rows_per_batch": peer_rows / max(1, n_batches),
