@@ -307,3 +307,25 @@ def test_gloo_two_rank_row_exchange():
         assert ok and same
         owners = [i % 2 for i in order]
         assert owners == sorted(owners)  # grouped by owner rank, stable
+
+
+def test_device_path_has_no_cpu_fallback(monkeypatch):
+    """The product path fails loudly without a GPU or without the extension:
+    no silent host or oracle fallback (the tier's parity rule)."""
+    import torch
+
+    from paper_2505_10806_b200 import _lib
+    import paper_2505_10806_b200 as rg
+
+    if torch.cuda.is_available():
+        pytest.skip("CPU-only check")
+    g = rg.synth_powerlaw(200, 3, 4, 3, 1)
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        rg.sample_block(g, np.array([0, 5, 9]), [3, 2], 11)
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        _lib.call("rg_mix64", None, None, 0, None)
+    # a missing shared library is an import-time error, not a fallback
+    monkeypatch.setattr(_lib, "_lib", None)
+    monkeypatch.setattr(_lib, "LIB_PATH", ROOT / "does_not_exist.so")
+    with pytest.raises(_lib.ExtensionMissing):
+        _lib.load()
