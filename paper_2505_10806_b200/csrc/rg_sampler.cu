@@ -271,35 +271,40 @@ __device__ __forceinline__ bool select_threshold(uint64_t nk, int D, int T, uint
   return true;
 }
 
-// PRNG-variant selection (rg_prng.cuh): Floyd's algorithm with the
-// generator replicated in every lane (warp-uniform draws); lane r < T ends
-// with the r-th drawn position (unsorted).
+// Lane-parallel Floyd for the PRNG variants: each lane runs the generator of
+// its own node; the n-th drawn position goes to col[n * kFloydStride] (a
+// per-warp [n][lane] table padded to 33 columns, so both this per-lane
+// column and the per-node row read back in phase B are bank-conflict free).
+constexpr int kFloydStride = 33;
+constexpr unsigned kVariantClaim = 32;  // one node per lane
+
 template <typename Gen>
-__device__ __forceinline__ int floyd_positions(Gen& g, int D, int T) {
-  const int lane = lane_id();
-  int mine = -1;
+__device__ __forceinline__ void floyd_lane(Gen& g, int D, int T, int32_t* col) {
+#pragma unroll 1
   for (int j = D - T, n = 0; j < D; ++j, ++n) {
     const int t = (int)g.bounded((uint32_t)(j + 1));
-    const bool dup = __ballot_sync(kFull, lane < n && mine == t) != 0u;
-    if (lane == n) mine = dup ? j : t;
+    bool dup = false;
+#pragma unroll 1
+    for (int i = 0; i < n; ++i) dup |= col[i * kFloydStride] == t;
+    col[n * kFloydStride] = dup ? j : t;
   }
-  return mine;
 }
 
-__device__ __forceinline__ int prng_positions(int prng, uint64_t nk, uint64_t sd, int D, int T) {
+__device__ __forceinline__ void prng_floyd_lane(int prng, uint64_t nk, uint64_t sd, int D, int T,
+                                                int32_t* col) {
   if (prng == kPcg32) {
     Pcg32 g;
     g.seed(nk, sd);
-    return floyd_positions(g, D, T);
-  }
-  if (prng == kSfc64) {
+    floyd_lane(g, D, T, col);
+  } else if (prng == kSfc64) {
     Sfc64 g;
     g.seed(nk, sd);
-    return floyd_positions(g, D, T);
+    floyd_lane(g, D, T, col);
+  } else {
+    Xoshiro256pp g;
+    g.seed(nk, sd);
+    floyd_lane(g, D, T, col);
   }
-  Xoshiro256pp g;
-  g.seed(nk, sd);
-  return floyd_positions(g, D, T);
 }
 
 // Per-node metadata (CSR row start, degree, id) for every frontier slot,
@@ -335,6 +340,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32)
   __shared__ uint64_t s_seed[kQueueBatches];  // step seed s_d of every batch
   __shared__ int32_t s_nf[kQueueBatches];     // frontier size of every batch
   __shared__ unsigned s_items;
+  __shared__ int32_t s_fl[kVariants ? kSampleWarps * 32 * kFloydStride : 1];  // Floyd draws
   const int lane = lane_id();
   const int warp = threadIdx.x >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
@@ -365,6 +371,79 @@ __global__ void __launch_bounds__(kSampleWarps * 32)
     if (lane == 0) t0 = atomicAdd(queue, claim);
     t0 = __shfl_sync(kFull, t0, 0);
     if (t0 >= items) break;
+    if constexpr (kVariants) {
+      // phase A, one item per lane: decode, count, and Floyd's draws for
+      // D > F in the lane's own generator (the draws are sequential per
+      // node, so a warp-uniform generator would run them 32 times over)
+      int32_t* s_flw = s_fl + warp * (32 * kFloydStride);
+      const unsigned k = t0 + lane;
+      bool live = false;
+      int D = 0, b = 0;
+      int64_t row = 0, a = 0;
+      if (k < items && lane < (int)claim) {
+        const int j = (int)(k / (unsigned)G);
+        b = (int)(k - (unsigned)j * (unsigned)G);
+        if (j < (b < kQueueBatches ? s_nf[b] : __ldg(nfront + b))) {
+          row = (int64_t)b * cap_in + j;
+          int32_t v;
+          if (meta) {
+            const int4 m = __ldg(meta + row);
+            a = (int64_t)(((uint64_t)(uint32_t)m.y << 32) | (uint32_t)m.x);
+            D = m.z;
+            v = m.w;
+          } else {
+            v = front[row];
+            a = indptr[v];
+            D = (int)(indptr[v + 1] - a);
+          }
+          const int T = min(D, F);
+          cnt[row] = T;
+          if (T > 32) {  // only reachable with fanout > 32: block path
+            const int at = atomicAdd(slow, 1);
+            slow[1 + at] = (int)k;
+          } else {
+            live = true;
+            if (D > F) {
+              const uint64_t sd = step_seed(b);
+              const uint64_t nk = mix64(((uint64_t)v + 1ull) * GOLDEN ^ sd);
+              prng_floyd_lane(prng, nk, sd, D, T, s_flw + lane);
+            }
+          }
+        }
+      }
+      __syncwarp();
+      // phase B, warp per item: neighbour loads, ascending emission, marks
+      unsigned todo = __ballot_sync(kFull, live);
+      while (todo) {
+        const int src = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const int64_t r_row = __shfl_sync(kFull, row, src);
+        const int64_t r_a = __shfl_sync(kFull, a, src);
+        const int r_D = __shfl_sync(kFull, D, src);
+        const int r_b = __shfl_sync(kFull, b, src);
+        const int r_T = min(r_D, F);
+        int32_t x = INT_MAX;
+        if (r_D > F) {
+          int p = lane < r_T ? s_flw[lane * kFloydStride + src] : INT_MAX;
+          if (sorted_rows) {
+            warp_bitonic_sort_keys(p);
+            if (lane < r_T) x = __ldg(indices + r_a + p);
+          } else {
+            if (lane < r_T) x = __ldg(indices + r_a + p);
+            warp_bitonic_sort_keys(x);
+          }
+        } else {  // D <= F <= 32: the whole row
+          if (lane < r_D) x = __ldg(indices + r_a + lane);
+          if (!sorted_rows) warp_bitonic_sort_keys(x);
+        }
+        if (lane < r_T) {
+          ell[r_row * F + lane] = x;
+          mark(bm + (int64_t)r_b * nwords, x);
+        }
+      }
+      __syncwarp();  // the next claim reuses s_flw
+      continue;
+    }
   // one division per claim; consecutive items step (j, b) with a wrap
   int j = (int)(t0 / (unsigned)G);
   int b = (int)(t0 - (unsigned)j * (unsigned)G) - 1;
@@ -400,25 +479,6 @@ __global__ void __launch_bounds__(kSampleWarps * 32)
     }
     int32_t* out = ell + row * F;
     uint32_t* bmb = bm + (int64_t)b * nwords;
-    if (kVariants && D > F) {
-      const uint64_t sd = step_seed(b);
-      const uint64_t nk = mix64(((uint64_t)v + 1ull) * GOLDEN ^ sd);
-      int p = prng_positions(prng, nk, sd, D, T);
-      int32_t x = INT_MAX;
-      if (sorted_rows) {
-        if (lane >= T) p = INT_MAX;
-        warp_bitonic_sort_keys(p);
-        if (lane < T) x = __ldg(indices + a + p);
-      } else {
-        if (lane < T) x = __ldg(indices + a + p);
-        warp_bitonic_sort_keys(x);
-      }
-      if (lane < T) {
-        out[lane] = x;
-        mark(bmb, x);
-      }
-      continue;
-    }
     if (D <= 32) {
       // one chunk: lane p owns position p.  The row (<= 128 B, the same
       // sectors a selective load would touch) is loaded before the keys are
@@ -821,7 +881,8 @@ extern "C" int rg_sample_level(const int64_t* d_indptr, const int32_t* d_indices
   if (slow && cudaMemsetAsync(slow, 0, sizeof(int32_t), s) != cudaSuccess)
     return check_launch("sample_level memset");
   RG_REQUIRE(d_meta != nullptr, "rg_sample_level: d_meta scratch is required");
-  RG_REQUIRE((uint64_t)G * (uint64_t)cap_in < (1ull << 32) - kClaim,
+  // headroom: every warp adds one claim past the end before it stops
+  RG_REQUIRE((uint64_t)G * (uint64_t)cap_in < (1ull << 32) - (1ull << 24),
              "rg_sample_level: G * cap_in above the 32-bit work queue");
   int4* meta = reinterpret_cast<int4*>(d_meta);
   // launch-wide work queue: the extra record after the G*cap_in meta records
@@ -837,18 +898,22 @@ extern "C" int rg_sample_level(const int64_t* d_indptr, const int32_t* d_indices
     const char* e = getenv("RG_SAMPLER_CLAIM");
     return e ? (unsigned)std::max(1, atoi(e)) : kClaim;
   }();
-  // one wave: 48 regs x 256 threads = 5 CTAs per SM (4 for the PRNG variants;
-  // capping at 40 regs for 6/SM measured 1-2 % slower);
+  // one wave: 48 regs x 256 threads = 5 CTAs per SM (capping at 40 regs for
+  // 6/SM measured 1-2 % slower; the PRNG variants at 4/SM: -1.2 %);
   // SplitMix64 keys (the reference) and the PRNG variants are separate
   // instantiations so the reference path keeps its register budget
+  static const int vctas = [] {
+    const char* e = getenv("RG_SAMPLER_VCTAS");
+    return e ? std::max(1, std::min(5, atoi(e))) : 5;
+  }();
   if (prng == kSplitMix)
     sample_level_kernel<false><<<kNumSMs * 5, kSampleWarps * 32, 0, s>>>(
         d_indptr, d_indices, G, d_front, meta, cap_in, d_nfront, fanout, level_mix, d_rng_seed,
         d_ell, d_cnt, d_bm, nwords, slow, sorted_rows, prng, queue, claim);
   else
-    sample_level_kernel<true><<<kNumSMs * 4, kSampleWarps * 32, 0, s>>>(
+    sample_level_kernel<true><<<kNumSMs * vctas, kSampleWarps * 32, 0, s>>>(
         d_indptr, d_indices, G, d_front, meta, cap_in, d_nfront, fanout, level_mix, d_rng_seed,
-        d_ell, d_cnt, d_bm, nwords, slow, sorted_rows, prng, queue, claim);
+        d_ell, d_cnt, d_bm, nwords, slow, sorted_rows, prng, queue, kVariantClaim);
   int rc = check_launch("sample_level");
   if (rc || !slow) return rc;
   sample_slow_kernel<<<kNumSMs, 256, 0, s>>>(d_indptr, d_indices, G, d_front, cap_in, fanout,
