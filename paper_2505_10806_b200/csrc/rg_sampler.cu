@@ -31,9 +31,10 @@ constexpr int kCompactThreads = 256;
 constexpr int kScanElems = 1024;          // elements per ELL-scan CTA
 constexpr int kFloydBits = 65536;         // PRNG slow path: largest degree with fanout > 32
 constexpr int kQueueBatches = 128;        // largest group G of one rg_sample_level call
-// items a warp claims from the launch queue per atomic (Products, batches/s:
-// 1 7,139; 2 8,267; 4 8,713; 8 8,843; 16 8,702)
-constexpr unsigned kClaim = 8;
+// items a warp claims from the launch queue per atomic, decoded one per lane
+// (Products G = 128, batches/s: 8 12,386; 12 12,404; 16 12,321; 20 12,236;
+// 24 12,148; 32 11,924; the earlier per-item warp decode at 8: 12,054)
+constexpr unsigned kClaim = 12;
 
 __device__ __forceinline__ void mark(uint32_t* bm, int32_t v) {
   atomicOr(bm + (v >> 5), 1u << (v & 31));
@@ -366,54 +367,124 @@ __global__ void __launch_bounds__(kSampleWarps * 32)
   auto step_seed = [&](int b) {
     return b < kQueueBatches ? s_seed[b] : mix64(__ldg(rng_seed + b) ^ level_mix);
   };
+  // one frontier node, warp-cooperative: select, emit ascending, mark
+  auto sample_node = [&](int64_t row, int64_t a, int D, int b, int32_t v) {
+    const int T = min(D, F);
+      int32_t* out = ell + row * F;
+      uint32_t* bmb = bm + (int64_t)b * nwords;
+      if (D <= 32) {
+        // one chunk: lane p owns position p.  The row (<= 128 B, the same
+        // sectors a selective load would touch) is loaded before the keys are
+        // computed, so its latency hides under the selection ALU work.
+        const int32_t row_nb = lane < D ? __ldg(indices + a + lane) : INT_MAX;
+        unsigned sel;
+        if (D <= F) {
+          sel = D == 32 ? kFull : ((1u << D) - 1u);
+        } else {
+          const uint64_t sd = step_seed(b);
+          const uint64_t nk = mix64(((uint64_t)v + 1ull) * GOLDEN ^ sd);
+          const uint64_t key = lane < D ? mix64(nk + (uint64_t)(lane + 1) * GOLDEN) : ~0ull;
+          sel = select_mask32(key, __ballot_sync(kFull, lane < D), T);
+        }
+        const bool mine = (sel >> lane) & 1u;
+        int32_t nb = mine ? row_nb : INT_MAX;
+        if (sorted_rows) {
+          // ascending CSR row: position order is id order
+          if (mine) {
+            out[__popc(sel & lt_mask)] = nb;
+            mark(bmb, nb);
+          }
+          return;
+        }
+        warp_bitonic_sort_keys(nb);
+        if (lane < T) {
+          out[lane] = nb;
+          mark(bmb, nb);
+        }
+        return;
+      }
+      // D > 32 (> F): threshold candidates, else the running top-T list
+      const uint64_t sd = step_seed(b);
+      const uint64_t nk = mix64(((uint64_t)v + 1ull) * GOLDEN ^ sd);
+      int pos;
+      const bool ordered = select_threshold(nk, D, F, s_key[warp], s_pos[warp], pos);  // T == F here
+      if (!ordered) pos = select_positions(nk, D, T);
+      int32_t nb = INT_MAX;
+      if (sorted_rows) {
+        int p = lane < T ? pos : INT_MAX;
+        if (!ordered) warp_bitonic_sort_keys(p);
+        if (lane < T) {
+          nb = __ldg(indices + a + p);
+          out[lane] = nb;
+          mark(bmb, nb);
+        }
+        return;
+      }
+      if (lane < T) nb = __ldg(indices + a + pos);
+      warp_bitonic_sort_keys(nb);
+      if (lane < T) {
+        out[lane] = nb;
+        mark(bmb, nb);
+      }
+  };
   for (;;) {
     unsigned t0 = 0;
     if (lane == 0) t0 = atomicAdd(queue, claim);
     t0 = __shfl_sync(kFull, t0, 0);
     if (t0 >= items) break;
-    if constexpr (kVariants) {
-      // phase A, one item per lane: decode, count, and Floyd's draws for
-      // D > F in the lane's own generator (the draws are sequential per
-      // node, so a warp-uniform generator would run them 32 times over)
-      int32_t* s_flw = s_fl + warp * (32 * kFloydStride);
-      const unsigned k = t0 + lane;
-      bool live = false;
-      int D = 0, b = 0;
-      int64_t row = 0, a = 0;
-      if (k < items && lane < (int)claim) {
-        const int j = (int)(k / (unsigned)G);
-        b = (int)(k - (unsigned)j * (unsigned)G);
-        if (j < (b < kQueueBatches ? s_nf[b] : __ldg(nfront + b))) {
-          row = (int64_t)b * cap_in + j;
-          int32_t v;
-          if (meta) {
-            const int4 m = __ldg(meta + row);
-            a = (int64_t)(((uint64_t)(uint32_t)m.y << 32) | (uint32_t)m.x);
-            D = m.z;
-            v = m.w;
-          } else {
-            v = front[row];
-            a = indptr[v];
-            D = (int)(indptr[v + 1] - a);
-          }
-          const int T = min(D, F);
-          cnt[row] = T;
-          if (T > 32) {  // only reachable with fanout > 32: block path
-            const int at = atomicAdd(slow, 1);
-            slow[1 + at] = (int)k;
-          } else {
-            live = true;
-            if (D > F) {
-              const uint64_t sd = step_seed(b);
-              const uint64_t nk = mix64(((uint64_t)v + 1ull) * GOLDEN ^ sd);
-              prng_floyd_lane(prng, nk, sd, D, T, s_flw + lane);
-            }
-          }
+    // phase A, one item per lane: decode, meta load and count for the
+    // claim's items at once (and, for the PRNG variants, Floyd's draws in
+    // the lane's own generator: they are sequential per node, so a
+    // warp-uniform generator would run them 32 times over)
+    const unsigned k = t0 + lane;
+    bool live = false;
+    int D = 0, b = 0;
+    int32_t v = 0;
+    int64_t row = 0, a = 0;
+    if (k < items && lane < (int)claim) {
+      const int j = (int)(k / (unsigned)G);
+      b = (int)(k - (unsigned)j * (unsigned)G);
+      if (j < (b < kQueueBatches ? s_nf[b] : __ldg(nfront + b))) {
+        row = (int64_t)b * cap_in + j;
+        if (meta) {
+          const int4 m = __ldg(meta + row);
+          a = (int64_t)(((uint64_t)(uint32_t)m.y << 32) | (uint32_t)m.x);
+          D = m.z;
+          v = m.w;
+        } else {
+          v = front[row];
+          a = indptr[v];
+          D = (int)(indptr[v + 1] - a);
         }
+        const int T = min(D, F);
+        cnt[row] = T;
+        if (T > 32) {  // only reachable with fanout > 32: block path
+          const int at = atomicAdd(slow, 1);
+          slow[1 + at] = (int)k;
+        } else {
+          live = true;
+        }
+      }
+    }
+    unsigned todo = __ballot_sync(kFull, live);
+    if constexpr (!kVariants) {
+      // phase B: the warp samples the live items one by one
+      while (todo) {
+        const int src = __ffs(todo) - 1;
+        todo &= todo - 1;
+        sample_node(__shfl_sync(kFull, row, src), __shfl_sync(kFull, a, src),
+                    __shfl_sync(kFull, D, src), __shfl_sync(kFull, b, src),
+                    __shfl_sync(kFull, v, src));
+      }
+    } else {
+      int32_t* s_flw = s_fl + warp * (32 * kFloydStride);
+      if (live && D > F) {
+        const uint64_t sd = step_seed(b);
+        const uint64_t nk = mix64(((uint64_t)v + 1ull) * GOLDEN ^ sd);
+        prng_floyd_lane(prng, nk, sd, D, F, s_flw + lane);  // T == F here
       }
       __syncwarp();
       // phase B, warp per item: neighbour loads, ascending emission, marks
-      unsigned todo = __ballot_sync(kFull, live);
       while (todo) {
         const int src = __ffs(todo) - 1;
         todo &= todo - 1;
@@ -442,98 +513,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32)
         }
       }
       __syncwarp();  // the next claim reuses s_flw
-      continue;
     }
-  // one division per claim; consecutive items step (j, b) with a wrap
-  int j = (int)(t0 / (unsigned)G);
-  int b = (int)(t0 - (unsigned)j * (unsigned)G) - 1;
-#pragma unroll 1
-  for (unsigned k = t0; k < t0 + claim && k < items; ++k) {
-    if (++b == G) {
-      b = 0;
-      ++j;
-    }
-    if (j >= (b < kQueueBatches ? s_nf[b] : __ldg(nfront + b))) continue;
-    const int64_t row = (int64_t)b * cap_in + j;
-    int32_t v;
-    int64_t a;
-    int D;
-    if (meta) {
-      const int4 m = __ldg(meta + row);
-      a = (int64_t)(((uint64_t)(uint32_t)m.y << 32) | (uint32_t)m.x);
-      D = m.z;
-      v = m.w;
-    } else {
-      v = front[row];
-      a = indptr[v];
-      D = (int)(indptr[v + 1] - a);
-    }
-    const int T = min(D, F);
-    if (lane == 0) cnt[row] = T;
-    if (T > 32) {  // only reachable with fanout > 32: block path below
-      if (lane == 0) {
-        int at = atomicAdd(slow, 1);
-        slow[1 + at] = (int)k;
-      }
-      continue;
-    }
-    int32_t* out = ell + row * F;
-    uint32_t* bmb = bm + (int64_t)b * nwords;
-    if (D <= 32) {
-      // one chunk: lane p owns position p.  The row (<= 128 B, the same
-      // sectors a selective load would touch) is loaded before the keys are
-      // computed, so its latency hides under the selection ALU work.
-      const int32_t row_nb = lane < D ? __ldg(indices + a + lane) : INT_MAX;
-      unsigned sel;
-      if (D <= F) {
-        sel = D == 32 ? kFull : ((1u << D) - 1u);
-      } else {
-        const uint64_t sd = step_seed(b);
-        const uint64_t nk = mix64(((uint64_t)v + 1ull) * GOLDEN ^ sd);
-        const uint64_t key = lane < D ? mix64(nk + (uint64_t)(lane + 1) * GOLDEN) : ~0ull;
-        sel = select_mask32(key, __ballot_sync(kFull, lane < D), T);
-      }
-      const bool mine = (sel >> lane) & 1u;
-      int32_t nb = mine ? row_nb : INT_MAX;
-      if (sorted_rows) {
-        // ascending CSR row: position order is id order
-        if (mine) {
-          out[__popc(sel & lt_mask)] = nb;
-          mark(bmb, nb);
-        }
-        continue;
-      }
-      warp_bitonic_sort_keys(nb);
-      if (lane < T) {
-        out[lane] = nb;
-        mark(bmb, nb);
-      }
-      continue;
-    }
-    // D > 32 (> F): threshold candidates, else the running top-T list
-    const uint64_t sd = step_seed(b);
-    const uint64_t nk = mix64(((uint64_t)v + 1ull) * GOLDEN ^ sd);
-    int pos;
-    const bool ordered = select_threshold(nk, D, F, s_key[warp], s_pos[warp], pos);  // T == F here
-    if (!ordered) pos = select_positions(nk, D, T);
-    int32_t nb = INT_MAX;
-    if (sorted_rows) {
-      int p = lane < T ? pos : INT_MAX;
-      if (!ordered) warp_bitonic_sort_keys(p);
-      if (lane < T) {
-        nb = __ldg(indices + a + p);
-        out[lane] = nb;
-        mark(bmb, nb);
-      }
-      continue;
-    }
-    if (lane < T) nb = __ldg(indices + a + pos);
-    warp_bitonic_sort_keys(nb);
-    if (lane < T) {
-      out[lane] = nb;
-      mark(bmb, nb);
-    }
-  }  // items of the claim
   }  // claims
 }
 
@@ -896,7 +876,7 @@ extern "C" int rg_sample_level(const int64_t* d_indptr, const int32_t* d_indices
   }
   static const unsigned claim = [] {
     const char* e = getenv("RG_SAMPLER_CLAIM");
-    return e ? (unsigned)std::max(1, atoi(e)) : kClaim;
+    return e ? (unsigned)std::max(1, std::min(32, atoi(e))) : kClaim;
   }();
   // one wave: 48 regs x 256 threads = 5 CTAs per SM (capping at 40 regs for
   // 6/SM measured 1-2 % slower; the PRNG variants at 4/SM: -1.2 %);
