@@ -33,8 +33,9 @@ constexpr int kFloydBits = 65536;         // PRNG slow path: largest degree with
 constexpr int kQueueBatches = 128;        // largest group G of one rg_sample_level call
 // items a warp claims from the launch queue per atomic, decoded one per lane
 // (Products G = 128, batches/s: 8 12,386; 12 12,404; 16 12,321; 20 12,236;
-// 24 12,148; 32 11,924; the earlier per-item warp decode at 8: 12,054)
-constexpr unsigned kClaim = 12;
+// 24 12,148; 32 11,924; the earlier per-item warp decode at 8: 12,054;
+// another box: 10 12,796; 12 12,716; 14 12,698)
+constexpr unsigned kClaim = 10;
 
 __device__ __forceinline__ void mark(uint32_t* bm, int32_t v) {
   atomicOr(bm + (v >> 5), 1u << (v & 31));
@@ -277,7 +278,7 @@ __device__ __forceinline__ bool select_threshold(uint64_t nk, int D, int T, uint
 // per-warp [n][lane] table padded to 33 columns, so both this per-lane
 // column and the per-node row read back in phase B are bank-conflict free).
 constexpr int kFloydStride = 33;
-constexpr unsigned kVariantClaim = 32;  // one node per lane
+constexpr unsigned kVariantClaim = 32;  // one node per lane (pcg32: 8 12,322; 16 13,203; 32 13,585)
 
 template <typename Gen>
 __device__ __forceinline__ void floyd_lane(Gen& g, int D, int T, int32_t* col) {
@@ -882,6 +883,10 @@ extern "C" int rg_sample_level(const int64_t* d_indptr, const int32_t* d_indices
   // 6/SM measured 1-2 % slower; the PRNG variants at 4/SM: -1.2 %);
   // SplitMix64 keys (the reference) and the PRNG variants are separate
   // instantiations so the reference path keeps its register budget
+  static const unsigned vclaim = [] {
+    const char* e = getenv("RG_SAMPLER_VCLAIM");
+    return e ? (unsigned)std::max(1, std::min(32, atoi(e))) : kVariantClaim;
+  }();
   static const int vctas = [] {
     const char* e = getenv("RG_SAMPLER_VCTAS");
     return e ? std::max(1, std::min(5, atoi(e))) : 5;
@@ -893,7 +898,7 @@ extern "C" int rg_sample_level(const int64_t* d_indptr, const int32_t* d_indices
   else
     sample_level_kernel<true><<<kNumSMs * vctas, kSampleWarps * 32, 0, s>>>(
         d_indptr, d_indices, G, d_front, meta, cap_in, d_nfront, fanout, level_mix, d_rng_seed,
-        d_ell, d_cnt, d_bm, nwords, slow, sorted_rows, prng, queue, kVariantClaim);
+        d_ell, d_cnt, d_bm, nwords, slow, sorted_rows, prng, queue, vclaim);
   int rc = check_launch("sample_level");
   if (rc || !slow) return rc;
   sample_slow_kernel<<<kNumSMs, 256, 0, s>>>(d_indptr, d_indices, G, d_front, cap_in, fanout,
