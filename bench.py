@@ -66,6 +66,9 @@ def parse():
     ap.add_argument("--prng", default="splitmix",
                     choices=["splitmix", "pcg32", "sfc64", "xoshiro256pp"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--train-groups", type=int, default=4,
+                    help="e2e_train leg: groups of 32 batches trained, overlapped vs serial "
+                         "(0: skip)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--nvtx", action="store_true", help="NVTX range 'timed' around the timed steps")
@@ -78,9 +81,6 @@ def parse():
                          "NCCL all-to-alls, ids out and rows back (nccl; spans nodes)")
     ap.add_argument("--pull", action="store_true",
                     help="N>1: every batch pulls its peer rows over NVLink (no group prefetch)")
-    ap.add_argument("--staged", action="store_true",
-                    help="N>1: owners stage their rows per 32-row chunk and consumers read "
-                         "them contiguously (measured slower than random pulls; DESIGN.md §9)")
     ap.add_argument("--graphs", action="store_true",
                     help="replay each group's launches from a captured CUDA graph (serial)")
     return ap.parse_args()
@@ -102,6 +102,72 @@ def build_inputs(cfg):
     book = partition_edgecut(g, cfg["parts"])
     log(f"[bench] inputs: n={g.num_nodes} E={g.num_edges} in {time.time() - t:.1f}s")
     return g, book
+
+
+def build_inputs_oracle(cfg):
+    """The same graph and partition from the CPU oracle (oracle/oracle_graph.c,
+    pinned to the reference's hashes): the reference arm never loads the
+    product library."""
+    from oracle import graph_oracle as go
+
+    t = time.time()
+    g = go.synth_powerlaw(cfg["n"], cfg["m"], cfg["d"], S0)
+    owner = go.partition_edgecut(g, cfg["parts"])
+    log(f"[bench] oracle inputs: n={g.num_nodes} E={g.num_edges} in {time.time() - t:.1f}s")
+    return g, owner
+
+
+def reference_hot_set(cfg, args, g, owner, part=0):
+    """Worker `part`'s steady hot set for epoch 0 at --cache-pct, as the
+    reference computes it (collect_access -> top_hot, plan.py:117-141;
+    n_hot = int(#remote * pct / 100), train.py:165-168).  Products worker 0
+    at 15 %: the set the reference itself produced (tests/golden/
+    products_w0.npz, made by tests/golden/make_golden_products.py); other
+    cases: the oracle over every batch of the epoch on the host cores."""
+    gold = ROOT / "tests" / "golden"
+    if (args.config == "products" and part == 0 and args.cache_pct == 15.0
+            and args.prng == "splitmix" and (gold / "products_w0.npz").exists()):
+        meta = json.loads((gold / "products.json").read_text())["workers"]["0"]["hot"]["15"]
+        hot = np.cumsum(np.load(gold / "products_w0.npz")["hot15_delta"].astype(np.int64))
+        assert len(hot) == meta["n_hot"]
+        return hot, meta["n_hot"], "reference (tests/golden/products_w0.npz)"
+    from oracle import gnn_oracle as orc
+
+    train = np.flatnonzero(g.train_mask)
+    nb = -(-len(train) // cfg["batch"])
+    state = cpu_state(g, owner, cfg, None, part)
+    ctx = mp.get_context("fork")
+    with ctx.Pool(os.cpu_count() or 1, initializer=_cpu_init, initargs=(state,)) as pool:
+        sets = pool.map(_cpu_inputs, range(nb), chunksize=4)
+    ids, counts = orc.access_counts(sets, owner, part)
+    n_hot = int(len(ids) * args.cache_pct / 100.0)
+    return orc.hot_set(ids, counts, n_hot), n_hot, "oracle plan pass (host)"
+
+
+class UnionCounter:
+    """|union of a group's input sets| on the device (rg_group_union with an
+    all-ones mask over the sampler's level-L bitmaps, then a popcount): the
+    distinct source rows one gather launch has to read at least once."""
+
+    def __init__(self, nwords: int):
+        import torch
+
+        self.nw = nwords
+        self.mask = torch.full((nwords,), -1, dtype=torch.int32, device="cuda")
+        self.out = torch.empty(nwords, dtype=torch.int32, device="cuda")
+        self.lut = torch.tensor([bin(i).count("1") for i in range(256)], dtype=torch.int64,
+                                device="cuda")
+        self.counts = []
+
+    def add(self, smp, ng: int) -> None:
+        from paper_2505_10806_b200 import _lib
+
+        _lib.call("rg_group_union", smp.bm.data_ptr(), self.nw, ng, self.mask.data_ptr(),
+                  self.out.data_ptr(), _lib.stream_handle())
+        self.counts.append(self.lut[self.out.view(dtype=__import__("torch").uint8).long()].sum())
+
+    def total(self) -> int:
+        return int(sum(int(c.item()) for c in self.counts))
 
 
 # ---------------------------------------------------------------- clocks
@@ -219,13 +285,23 @@ def _cpu_batch(i: int) -> int:
     return int(rows.shape[0])
 
 
-def cpu_state(g, book, cfg, hot_ids, part=0):
+def _cpu_inputs(i: int) -> np.ndarray:
+    """input_nodes of batch i (oracle sample_block)."""
+    from oracle import gnn_oracle as orc
+
+    st = _CPU
+    seeds = st["perm"][i * st["batch"]:(i + 1) * st["batch"]]
+    fr, _ = orc.block(st["indptr"], st["indices"], seeds, st["fanouts"], orc.batch_seed(S0, 0, i))
+    return fr[-1]
+
+
+def cpu_state(g, owner, cfg, hot_ids, part=0):
     from oracle import gnn_oracle as orc
 
     train = np.flatnonzero(g.train_mask)
     return {"perm": orc.epoch_order(train, S0, 0), "batch": cfg["batch"], "indptr": g.indptr,
             "indices": g.indices, "fanouts": cfg["fanouts"], "features": g.features,
-            "owner": book.owner, "part": part, "hot": hot_ids}
+            "owner": np.asarray(owner), "part": part, "hot": hot_ids}
 
 
 def cpu_baseline(state, seconds: float, nb: int):
@@ -251,14 +327,31 @@ def cpu_baseline(state, seconds: float, nb: int):
 
 
 # ---------------------------------------------------------------- reference arm
+def workload_config(args, cfg, part, n_hot) -> dict:
+    """The `config` both arms print: the workload only (identical keys and
+    values for the same workload, so the driver can pair the arms)."""
+    return {"workload": args.config, "batch_size": cfg["batch"], "fanouts": cfg["fanouts"],
+            "partitions": cfg["parts"], "worker": part, "cache_pct": args.cache_pct,
+            "n_hot": int(n_hot), "prng": args.prng}
+
+
 def run_reference(args, cfg):
+    """The reference's own CPU implementation of the path on the host cores:
+    the oracle port of the producer body (sample_block + assemble_bundle of
+    worker 0 with the epoch's steady 15 % hot cache, prefetch.py:123-125) —
+    the reference itself is pure Python and cannot travel to the GPU box.
+    Inputs come from the C oracle generator; nothing loads the product
+    library.  One step = one batch per host core (forked processes)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    g, book = build_inputs(cfg)
-    # uncached baseline mode: every remote row is a fallback pull (the copy
-    # work per batch is the same as with a cache)
-    state = cpu_state(g, book, cfg, np.empty(0, np.int64))
+    if cfg.get("device_features"):
+        emit({"impl": "reference", "unavailable": "papers100M-shaped features are generated on "
+                                                  "the device; no host feature table to read"})
+        return
+    g, owner = build_inputs_oracle(cfg)
+    hot, n_hot, hot_src = reference_hot_set(cfg, args, g, owner, 0)
+    state = cpu_state(g, owner, cfg, hot, 0)
     _cpu_init(state)
     cores = os.cpu_count() or 1
     nb = -(-int(g.train_mask.sum()) // cfg["batch"])
@@ -277,16 +370,24 @@ def run_reference(args, cfg):
     line = {"metric": METRIC, "value": value, "unit": "batches/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
-            "data": "synthetic (gnnpipe.synth_powerlaw shape, bit-identical native generator)",
+            "data": (f"synthetic: gnnpipe.synth_powerlaw({cfg['n']}, {cfg['m']}, {cfg['d']}, "
+                     f"{cfg['classes']}, seed={S0}) + partition_edgecut(k={cfg['parts']}), "
+                     f"from the C oracle (oracle/oracle_graph.c, hash-pinned)"),
             "impl": "reference",
-            "config": {"workload": args.config, "batch_size": cfg["batch"],
-                       "fanouts": cfg["fanouts"], "partitions": cfg["parts"],
-                       "batches_per_step": cores, "cache": "none (baseline mode)"},
+            "config": workload_config(args, cfg, 0, n_hot),
+            "batches_per_step": cores, "parallelism": f"{cores} forked host processes",
+            "hot_set": hot_src,
             "cpu_baseline": {"value": value, "unit": "batches/s", "cores": cores, "kind": "port",
-                             "sample": f"{args.steps} steps x {cores} mini-batches, oracle port "
-                                       f"of sample_block + assemble_bundle, one per process"},
+                             "sample": f"{args.steps} steps x {cores} mini-batches of epoch 0 "
+                                       f"(oracle sample_block + bundle rows + accounting of "
+                                       f"worker 0 with its {n_hot}-row steady cache), one batch "
+                                       f"per process"},
             "e2e": {"value": value, "unit": "batches/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
+    # the reference arm must not touch the product: no module, no library
+    assert not any(m.startswith("paper_2505_10806_b200") for m in sys.modules)
+    with open("/proc/self/maps") as f:
+        assert "librapidgnn_b200" not in f.read()
     emit(line)
 
 
@@ -361,18 +462,16 @@ def main():
                                                      dg.device))
     if world > 1 and args.transport == "p2p":
         multigpu.exchange_shards(store, rank, world)
-    if args.transport == "nccl" and (args.pull or args.staged):
-        raise SystemExit("--transport nccl needs the group prefetch (no --pull / --staged)")
+    if args.transport == "nccl" and args.pull:
+        raise SystemExit("--transport nccl needs the group prefetch (no --pull)")
     store.build_route(shard_ids)
     train = np.flatnonzero(g.train_mask)
-    # --staged keeps a second full set of bundle-sized staging buffers: 32
-    group = args.group or (32 if args.staged else cfg.get("group", 32))
+    group = args.group or cfg.get("group", 32)
     pipe = WorkerPipeline(dg, store, part, train, cfg["fanouts"], cfg["batch"], S0, group,
                           nbuf=1 if (args.serial or args.graphs) else 2, prng=args.prng)
     nb, G = pipe.nb, pipe.G
     sched = SeedSchedule(S0, 1, nb)
-    staged = world > 1 and args.staged
-    if world > 1 and not args.pull and not staged:
+    if world > 1 and not args.pull:
         pipe.enable_prefetch(args.transport, rank, world)  # before the cache fill (nccl)
 
     # per-epoch part: plan pass (access counts), hot set, cache fill
@@ -396,13 +495,8 @@ def main():
     n_full = max(1, nb // G)
     smp = pipe.sampler
 
-    if staged:
-        pipe.enable_staging(rank, world)
-
     def step(kk, timed_events=None):
         i0 = (kk % n_full) * G
-        if staged:
-            return i0, pipe.step_staged(i0, dist.barrier, timed_events)
         if args.graphs:
             return i0, pipe.step_graph(i0)
         if not args.serial:
@@ -415,8 +509,10 @@ def main():
         pipe.gather(ng, i0)
         if timed_events is not None:
             timed_events[1].record()
+            unions.add(smp, ng)
         return i0, ng
 
+    unions = UnionCounter(dg.nwords)
     clk = Clocks(local).__enter__()  # under load from warm-up to the end of the epoch pass
     pipe.enter_streams()
     for kk in range(args.warmup):
@@ -471,7 +567,7 @@ def main():
             log(f"[timeline] rank {rank} {name:8s} slot {slot} "
                 f"{start.elapsed_time(e0):9.3f} -> {start.elapsed_time(e1):9.3f} ms")
         pipe.timeline = None
-    if staged or (args.serial and not args.graphs):
+    if args.serial and not args.graphs:
         gather_ms = sum(a.elapsed_time(b) for a, b in gev)
     else:
         # overlapped run: time the gather alone on the same batches (serial),
@@ -484,6 +580,7 @@ def main():
             ng = min(G, nb - i0)
             pipe.plan.fill(pipe.perm, 0, i0, ng)
             smp.run(ng)
+            unions.add(smp, ng)
             if flush:
                 scrub.fill_(float(kk))
             if pipe.prefetch:
@@ -530,14 +627,19 @@ def main():
     # roofline of the dominant kernel (bundle gather): read + write every row,
     # plus the id and route word per row
     peak, peak_src = peaks()
+    # per batch: read + write every row + its id and route word
     gather_bytes = timed_rows * (2 * 4 * d + 8)
-    achieved = gather_bytes / (gather_ms / 1e3) / 1e9
+    # per launch: every bundle row written once, every distinct source row of
+    # the group read once (the group's batches share rows, served from L2)
+    union_rows = unions.total()
+    launch_bytes = timed_rows * (4 * d + 8) + union_rows * 4 * d
+    achieved = launch_bytes / (gather_ms / 1e3) / 1e9
     step_bytes = gather_bytes  # sampler bytes reported in DESIGN.md (~3% of the batch)
 
     # e2e: host seeds in (pinned H2D), accounting out (D2H) per group
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(pipe, g, cfg, args, world, staged)
+        e2e = run_e2e(pipe, g, cfg, args, world)
 
     result = None
     check = run_check(pipe, g, cfg, S0, args.prng) if args.check else None
@@ -547,9 +649,19 @@ def main():
         dist.all_reduce(flags, op=dist.ReduceOp.MIN)
         check["all_ranks_bit_exact"] = bool(flags.item())
     e2e_rows = run_e2e_host_rows(pipe, cfg, args, world) if not args.no_e2e else None
+    hot_np = hot.cpu().numpy().astype(np.int64)
+    legs = {}
+    if world == 1 and not args.no_e2e and not cfg.get("device_features"):
+        legs["e2e_dropin"] = run_dropin(g, book, cfg, hot_np, part)
+        legs["q_bounded"] = run_group_leg(dg, store, part, train, cfg, hot, 2, 2, 256)
+        if args.train_groups:
+            legs["e2e_train"] = {
+                "overlapped": run_train_leg(dg, store, part, train, cfg, hot, g.labels, 32,
+                                            args.train_groups, True),
+                "serial": run_train_leg(dg, store, part, train, cfg, hot, g.labels, 32,
+                                        args.train_groups, False)}
     if rank == 0 and world == 1 and not args.no_cpu and not cfg.get("device_features"):
-        hot_np = hot.cpu().numpy().astype(np.int64)
-        result = cpu_baseline(cpu_state(g, book, cfg, hot_np, part), args.cpu_seconds, nb)
+        result = cpu_baseline(cpu_state(g, book.owner, cfg, hot_np, part), args.cpu_seconds, nb)
 
     traffic_b = ncu_traffic("gather_bundle_kernel", args.config, G)
     agg_batches = n_batches * world
@@ -567,34 +679,39 @@ def main():
         "data": (f"synthetic: gnnpipe.synth_powerlaw({cfg['n']}, {cfg['m']}, {cfg['d']}, "
                  f"{cfg['classes']}, seed={S0}) reproduced bit-exactly + "
                  f"partition_edgecut(k={k})"),
-        "config": {"workload": args.config, "batch_size": cfg["batch"], "fanouts": cfg["fanouts"],
-                   "partitions": k, "worker": part, "cache_pct": args.cache_pct, "n_hot": n_hot,
-                   "prng": args.prng,
-                   "batches_per_step": G, "parallelism": f"worker-per-gpu x{world}",
-                   "l2": ("L2 flushed between timed steps (feature table %.0f MB < 2x L2); "
-                          "steps timed individually" if flush else
-                          "inputs larger than L2 (feature shards %.0f MB; bundle %.0f MB/batch)")
-                         % ((feat_bytes / 1e6,) if flush
-                            else (feat_bytes / 1e6, float(rows_b.mean()) * d * 4 / 1e6))},
-        "roofline": {"kernel": "gather_queue_kernel (rg_gather_bundle)", "bound": "hbm", "achieved": achieved,
-                     "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+        "config": workload_config(args, cfg, part, n_hot),
+        "batches_per_step": G, "parallelism": f"worker-per-gpu x{world}",
+        "l2": ("L2 flushed between timed steps (feature table %.0f MB < 2x L2); "
+               "steps timed individually" if flush else
+               "inputs larger than L2 (feature shards %.0f MB; bundle %.0f MB/batch)")
+              % ((feat_bytes / 1e6,) if flush
+                 else (feat_bytes / 1e6, float(rows_b.mean()) * d * 4 / 1e6)),
+        "roofline": {"kernel": "gather_queue_kernel (rg_gather_bundle)", "bound": "hbm",
+                     "achieved": achieved, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic_b,
-                     "bytes_per_launch": gather_bytes / args.steps,
+                     "bytes_per_launch": launch_bytes / args.steps,
+                     "union_rows_per_launch": union_rows / args.steps,
+                     "bundle_rows_per_launch": timed_rows / args.steps,
+                     "ms_per_launch": gather_ms / args.steps,
                      "share_of_step": gather_ms / step_ms_local,
-                     "step_frac": step_bytes / (step_ms_local / 1e3) / 1e9 / peak,
                      "dram_achieved": (traffic_b / (gather_ms / args.steps / 1e3) / 1e9
                                        if traffic_b else None),
                      "dram_frac": (traffic_b / (gather_ms / args.steps / 1e3) / 1e9 / peak
                                    if traffic_b else None),
-                     "note": ("feature table fits in L2: rows reused by the step's batches hit "
-                              "L2 (L2 is flushed only between steps), so frac can exceed 1"
-                              if flush else
-                              "achieved = algorithmic bytes / time; the chunk-major gather queue "
-                              "serves rows shared by the step's batches from L2, so DRAM traffic "
-                              "is below the algorithmic bytes and frac exceeds 1; dram_achieved / "
-                              "dram_frac = measured DRAM bytes (ncu, traffic) / the same time")},
+                     "per_batch_bytes": {
+                         "bytes_per_launch": gather_bytes / args.steps,
+                         "gbs": gather_bytes / (gather_ms / 1e3) / 1e9,
+                         "step_frac": step_bytes / (step_ms_local / 1e3) / 1e9 / peak,
+                         "note": "every batch's rows counted as read from HBM (SURVEY.md §8d "
+                                 "per-batch figure); the group's shared rows come from L2, so "
+                                 "this exceeds the DRAM roofline by design"},
+                     "note": ("achieved = the launch's algorithmic bytes / its event-timed "
+                              "duration: bundle rows written + ids/routes + each distinct "
+                              "source row of the group read once; dram_frac = ncu DRAM bytes "
+                              "(traffic, profiles/traffic.json) / the same time")},
         "e2e": e2e,
         "e2e_host_rows": e2e_rows,
+        **legs,
         "nvlink": ({"mode": ("group prefetch (rg_prefetch_rows): each group's peer rows "
                              "copied once into local shadows, gather all-local"
                              if args.transport == "p2p" else
@@ -613,8 +730,8 @@ def main():
                              "NCCL transport: the prefetch time also contains waits for the "
                              "other ranks' matching collectives (ranks drift in the serial "
                              "re-timing loop), so achieved_gbs understates the link")}
-                   if world > 1 and pipe.prefetch and not staged else
-                   {"mode": "staged" if staged else "per-batch pull",
+                   if world > 1 and pipe.prefetch else
+                   {"mode": "per-batch pull",
                     "peer_rows_per_batch": peer_rows / max(1, n_batches),
                     "bytes_per_batch": peer_rows * 4 * d / max(1, n_batches),
                     "achieved_gbs": peer_rows * 4 * d / (gather_ms / 1e3) / 1e9,
@@ -676,6 +793,142 @@ def run_check(pipe, g, cfg, s0, prng="splitmix"):
             "rows_bit_exact": rows_ok, "oracle_s": round(time.time() - t, 1)}
 
 
+def run_dropin(g, book, cfg, hot_np, part, batches: int = 48, warm: int = 6):
+    """The reference-facing API end to end: Prefetcher(plan, ...) with the
+    worker's shard, a StoreClient over every shard and the steady cache,
+    exactly as train.py:208-221 drives it; every bundle's rows are read as
+    the numpy array the reference returns (FeatureBundle.rows).  One batch
+    per plan.block + assemble_bundle, producer thread Q = 3 ahead."""
+    import torch
+
+    import paper_2505_10806_b200 as rg
+
+    k, d = cfg["parts"], cfg["d"]
+    owner = np.asarray(book.owner)
+    train = np.flatnonzero(g.train_mask)
+    shards = [rg.StoreShard(q, np.flatnonzero(owner == q), g.features[owner == q])
+              for q in range(k)]
+    client = rg.StoreClient(owner, [rg.InprocTransport(s) for s in shards], d)
+    cache = rg.build_steady(hot_np, client, rg.TransferAccount())
+    plan = rg.generate_plan(g, train, cfg["fanouts"], cfg["batch"], 1, S0, keep_inputs=False,
+                            group=cfg.get("group", 32))
+    acct = rg.TransferAccount()
+    torch.cuda.synchronize()
+    pf = rg.Prefetcher(plan, 0, owner, part, shards[part], client, cache, acct, depth=3)
+    nbytes = 0
+    for _ in range(warm):
+        pf.next_bundle().rows
+    t = time.perf_counter()
+    for _ in range(batches):
+        b = pf.next_bundle()
+        nbytes += b.rows.nbytes
+    wall = time.perf_counter() - t
+    pf.drain()
+    del shards, client, cache
+    torch.cuda.empty_cache()
+    return {"value": batches / wall, "unit": "batches/s", "batches": batches,
+            "d2h_bytes_per_batch": nbytes / batches,
+            "api": "Prefetcher(plan, 0, owner, p, shard, client, cache, account, depth=3): "
+                   "plan.block + assemble_bundle per batch on a producer thread, "
+                   "FeatureBundle.rows (numpy) read by the consumer"}
+
+
+def run_group_leg(dg, store, part, train, cfg, hot, group: int, nbuf: int, steps: int):
+    """Memory-bounded configuration: G batches per step x nbuf slots live
+    bundles (G = 2, nbuf = 2: Q + 1 = 4 bundles, the reference's bound,
+    prefetch.py:1-7), overlapped, device-timed."""
+    import torch
+
+    from paper_2505_10806_b200.pipeline import WorkerPipeline
+    from paper_2505_10806_b200.sampler import SeedSchedule
+
+    pipe = WorkerPipeline(dg, store, part, train, cfg["fanouts"], cfg["batch"], S0, group,
+                          nbuf=nbuf)
+    pipe.build_cache(hot)
+    pipe.start_epoch(SeedSchedule(S0, 1, pipe.nb), 0)
+    pipe.enter_streams()
+    n_full = pipe.nb // group
+    for kk in range(8):
+        pipe.step_overlapped((kk % n_full) * group)
+    pipe.sync_streams()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    t0.record()
+    pipe.enter_streams()
+    for kk in range(steps):
+        pipe.step_overlapped(((8 + kk) % n_full) * group)
+    pipe.sync_streams()
+    t1.record()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    del pipe
+    torch.cuda.empty_cache()
+    return {"value": steps * group / (ms / 1e3), "unit": "batches/s", "batches_per_step": group,
+            "slots": nbuf, "live_bundles": group * nbuf, "steps": steps}
+
+
+def run_train_leg(dg, store, part, train, cfg, hot, labels_np, group: int, groups: int,
+                  overlap: bool):
+    """Consumer attached: every batch sampled + gathered AND trained (the
+    device GraphSAGE step of train.py: bit-exact aggregation, cuBLAS fp32
+    GEMMs, SGD), `groups` groups of `group` batches.  overlap=True: the
+    GroupProducer thread samples/gathers group k+1 on the side streams while
+    group k trains (prefetch.py:91-164); False: produce, then train, serially.
+    Wall-clock batches/s (the host enqueues the training step)."""
+    import torch
+
+    from paper_2505_10806_b200 import model
+    from paper_2505_10806_b200.pipeline import GroupProducer, WorkerPipeline
+    from paper_2505_10806_b200.sampler import SeedSchedule
+
+    torch.backends.cuda.matmul.allow_tf32 = False
+    d = cfg["d"]
+    pipe = WorkerPipeline(dg, store, part, train, cfg["fanouts"], cfg["batch"], S0, group,
+                          nbuf=2 if overlap else 1)
+    pipe.build_cache(hot)
+    pipe.start_epoch(SeedSchedule(S0, 1, pipe.nb), 0)
+    labels = torch.from_numpy(np.asarray(labels_np)).cuda()
+    params = model.init_params(d, 32, cfg["classes"], len(cfg["fanouts"]), 1234)
+    loss_sum = torch.zeros((), dtype=torch.float64, device="cuda")
+
+    def train_group(smp, rows_buf, ng, nf):
+        nonlocal params
+        for b in range(ng):
+            blk = model.block_from_slot(smp, b, nf[:, b])
+            rows = rows_buf[b, : int(nf[smp.L, b]), :d]
+            loss, grads = model.loss_and_grad(blk, rows, labels, params)
+            params = model.sgd_step(params, grads, 0.05)
+            loss_sum.add_(loss.double())
+
+    def epoch_part(starts):
+        if overlap:
+            prod = GroupProducer(pipe, starts)
+            try:
+                while (item := prod.next_group()) is not None:
+                    i0, ng, slot, nf = item
+                    train_group(pipe.samplers[slot], pipe.row_bufs[slot], ng, nf)
+                    prod.release(slot)
+            finally:
+                prod.close()
+        else:
+            for i0 in starts:
+                ng = pipe.step(i0)
+                train_group(pipe.sampler, pipe.rows, ng, pipe.sampler.nfront[:, :ng].cpu().numpy())
+
+    epoch_part([0])  # warm-up: allocator, cuBLAS handles
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    starts = [(1 + k) * group for k in range(groups)]
+    epoch_part(starts)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t
+    loss = float(loss_sum.item())
+    del pipe
+    torch.cuda.empty_cache()
+    return {"value": groups * group / wall, "unit": "batches/s", "batches": groups * group,
+            "group": group, "overlap": overlap, "loss_sum": loss}
+
+
 def run_e2e_host_rows(pipe, cfg, args, world):
     """Informational: the numpy-facing drop-in returns bundle rows on the
     host, so every batch's rows (the valid |input| x d part of its slot) are
@@ -725,7 +978,7 @@ def run_e2e_host_rows(pipe, cfg, args, world):
                    "2-batch pinned ring"}
 
 
-def run_e2e(pipe, g, cfg, args, world, staged=False):
+def run_e2e(pipe, g, cfg, args, world):
     """Public pipeline API with host buffers: each step copies the group's
     seed ids + batch seeds from pinned host memory (H2D), samples and
     gathers, and reads the per-batch accounting back (D2H, host-visible
@@ -734,9 +987,10 @@ def run_e2e(pipe, g, cfg, args, world, staged=False):
     import torch
     import torch.distributed as dist
 
-    from oracle import gnn_oracle as orc  # host batch seeds = BatchPlan.batch_seeds
+    from paper_2505_10806_b200.sampler import SeedSchedule, seed_for
 
     G, nb, smp = pipe.G, pipe.nb, pipe.sampler
+    sched = SeedSchedule(S0, 1, nb)
     B = cfg["batch"]
     perm = pipe.perm.cpu().numpy()
     n_full = max(1, nb // G)
@@ -749,9 +1003,9 @@ def run_e2e(pipe, g, cfg, args, world, staged=False):
             chunk = perm[i * B:(i + 1) * B]
             seeds_h[s, b, :len(chunk)] = torch.from_numpy(chunk.astype(np.int32))
             nseeds_h[s, b] = len(chunk)
-            rng_h[s, b] = int(np.uint64(orc.batch_seed(S0, 0, i)).astype(np.int64))
+            rng_h[s, b] = int(np.uint64(seed_for(sched, 0, i)).astype(np.int64))
     out_h = torch.zeros((G, 8), dtype=torch.int32).pin_memory()
-    overlapped = not staged and not args.serial and not args.graphs
+    overlapped = not args.serial and not args.graphs
     ring = [torch.zeros((G, 8), dtype=torch.int32).pin_memory() for _ in range(2)]
     ring_ev = [torch.cuda.Event() for _ in range(2)]
     pending = []
@@ -785,18 +1039,11 @@ def run_e2e(pipe, g, cfg, args, world, staged=False):
             return one_overlapped(kk)
         s = kk % n_full
         i0 = s * G
-        if staged:
-            tgt = pipe.samplers[pipe.k % 2 % pipe.nbuf]
-            tgt.seeds.copy_(seeds_h[s], non_blocking=True)
-            tgt.nseeds.copy_(nseeds_h[s], non_blocking=True)
-            tgt.rng.copy_(rng_h[s], non_blocking=True)
-            pipe.step_staged(i0, dist.barrier, fill=False)
-        else:
-            smp.seeds.copy_(seeds_h[s], non_blocking=True)
-            smp.nseeds.copy_(nseeds_h[s], non_blocking=True)
-            smp.rng.copy_(rng_h[s], non_blocking=True)
-            smp.run(G)
-            pipe.gather(G, i0)
+        smp.seeds.copy_(seeds_h[s], non_blocking=True)
+        smp.nseeds.copy_(nseeds_h[s], non_blocking=True)
+        smp.rng.copy_(rng_h[s], non_blocking=True)
+        smp.run(G)
+        pipe.gather(G, i0)
         out_h.copy_(pipe.counters[i0:i0 + G], non_blocking=True)
         torch.cuda.current_stream().synchronize()
         return int(out_h[:, 2].sum())

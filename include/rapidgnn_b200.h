@@ -184,35 +184,6 @@ int rg_gather_bundle(const int32_t* d_ids, const int32_t* d_nids, int64_t cap, i
                      int32_t stride, int32_t my_part, uint32_t peer_mask, float* d_out,
                      uint32_t* d_counters, void* stream);
 
-/* Staged multi-GPU mode.  Owner side: rows of the G slots whose route kind
- * is in mine_mask (the partitions this GPU holds, cached by consumers or
- * not) are copied to d_stage at their chunk-aligned slot
- * (b*cap + 32*w + k), k = rank of the row among chunk w's rows owned by
- * this GPU.  Consumer side: like rg_gather_bundle, but fallback rows owned
- * by a partition on another GPU (peer_mask) are read from that GPU's
- * staging buffer (h_stage[rank], IPC-mapped) at the same slot, so NVLink
- * reads are contiguous runs instead of random 400-B rows.  h_rank_of[16]:
- * partition -> rank; d_owner: uint8 partition of every node.  The caller
- * orders "all owners staged" before the consumer gather (host barrier).  */
-int rg_stage_rows(const int32_t* d_ids, const int32_t* d_nids, int64_t cap, int32_t G,
-                  const uint32_t* d_base_route, const float* const* h_bases, uint32_t mine_mask,
-                  int32_t src_stride, int32_t stride, float* d_stage, void* stream);
-int rg_gather_bundle_staged(const int32_t* d_ids, const int32_t* d_nids, int64_t cap, int32_t G,
-                            const uint32_t* d_route, const uint8_t* d_owner,
-                            const float* const* h_bases, const float* const* h_stage,
-                            const uint8_t* h_rank_of, int32_t my_rank, int32_t src_stride,
-                            int32_t stride, int32_t my_part, uint32_t peer_mask, float* d_out,
-                            uint32_t* d_counters, void* stream);
-
-/* Same contract, rows moved by TMA bulk copies (global -> smem -> global),
- * one warp per CTA, ctas_per_sm CTAs per SM (<= 0: default 4): in-flight
- * bytes live in shared memory, so the sampler can run concurrently on the
- * SMs' remaining warp slots and registers.  Rows up to ~1.5 KB.          */
-int rg_gather_bundle_tma(const int32_t* d_ids, const int32_t* d_nids, int64_t cap, int32_t G,
-                         const uint32_t* d_route, const float* const* h_bases,
-                         int32_t src_stride, int32_t stride, int32_t my_part, float* d_out,
-                         uint32_t* d_counters, int32_t ctas_per_sm, void* stream);
-
 /* ---- group prefetch of peer rows (north_star item 4) ---
  * bits[w] bit j = the route kind of node 32w+j is in kind_mask.         */
 int rg_route_kind_bits(const uint32_t* d_route, int64_t n, uint32_t kind_mask, uint32_t* d_bits,
@@ -236,26 +207,43 @@ int rg_scatter_rows(const int32_t* d_ids, int64_t n, const uint32_t* d_route,
                     int32_t dst_stride, int32_t d, void* stream);
 
 /* ---- L5 aggregation consumer (model.py:72-81, 126-135) -------------- */
-/* mean[t] = (sum over t's edges, in stored order, of h[pos(src)]) /
- * max(cnt_t, 1) and self[t] = h[pos(dst_front[t])], positions located by
- * binary search in the sorted src_front.  fp32, in-order, IEEE divide. */
-int rg_sage_mean_fwd(const float* d_h, int64_t n_src, int32_t H, int32_t ldh,
-                     const int32_t* d_src_front, const int32_t* d_dst_front, int64_t n_dst,
-                     const int32_t* d_ell, const int32_t* d_cnt, int32_t fanout, float* d_mean,
-                     float* d_self, int32_t* d_self_pos, void* stream);
+#define RG_DTYPE_F32 0 /* RunConfig.precision "f32" (train.py:117)          */
+#define RG_DTYPE_F64 1 /* RunConfig.precision "f64"                          */
+/* Positions of one level (model.py:53-55, 74-75, the searchsorted of src
+ * and dst into the sorted src frontier), resolved once and shared by the
+ * forward and the backward: d_rank is an n_nodes int32 scratch table
+ * (rank[src_front[j]] = j), d_epos[t*fanout + r] = position of the r-th
+ * sampled neighbour of dst row t (-1 for r >= cnt[t]), d_self_pos[t] =
+ * position of dst_front[t].  Frontiers are nested (dst ⊂ src) and every
+ * ELL entry is a member of src_front (the sampler's contract).          */
+int rg_sage_positions(const int32_t* d_src_front, int64_t n_src, const int32_t* d_dst_front,
+                      int64_t n_dst, const int32_t* d_ell, const int32_t* d_cnt, int32_t fanout,
+                      int64_t n_nodes, int32_t* d_rank, int32_t* d_epos, int32_t* d_self_pos,
+                      void* stream);
+/* mean[t] = (in stored order, sum of h[epos[t, r]]) / max(cnt_t, 1) and
+ * self[t] = h[self_pos[t]] (self may be NULL); h rows ldh elements apart,
+ * outputs dense [n_dst, H].  dtype RG_DTYPE_F32 / F64; in-order, IEEE
+ * divide: bit-exact with the reference's np.add.at / divide.            */
+int rg_sage_mean_fwd(int32_t dtype, const void* d_h, int32_t H, int32_t ldh,
+                     const int32_t* d_epos, const int32_t* d_self_pos, int64_t n_dst,
+                     const int32_t* d_cnt, int32_t fanout, void* d_mean, void* d_self,
+                     void* stream);
+/* Transposed edge index for the backward: edges grouped by src position,
+ * ascending dst row inside a group (the reference's edge order for that
+ * src), any group length.  d_toff n_src+1, d_tdst n_dst*fanout; scratch
+ * of rg_sage_transpose_scratch(...) BYTES (-1: sizes out of range).     */
+int64_t rg_sage_transpose_scratch(int64_t n_src, int64_t n_dst, int32_t fanout);
+int rg_sage_transpose(const int32_t* d_epos, const int32_t* d_cnt, int64_t n_dst, int32_t fanout,
+                      int64_t n_src, int32_t* d_toff, int32_t* d_tdst, void* d_scratch,
+                      int64_t scratch_bytes, void* stream);
 /* Backward scatter (model.py:126-135): dh = 0; dh[self_pos[t]] += dself[t];
  * then for each edge in (dst asc, src asc) order dh[pos(src)] +=
- * dmean[t] / max(cnt_t,1).  d_tpos/d_toff: transposed edge index built
- * by rg_sage_transpose (same order => deterministic, bit-exact).       */
-int64_t rg_sage_transpose_scratch(int64_t n_src, int64_t n_dst, int32_t fanout);
-int rg_sage_transpose(const int32_t* d_src_front, int64_t n_src, const int32_t* d_ell,
-                      const int32_t* d_cnt, int64_t n_dst, int32_t fanout, int32_t* d_toff,
-                      int32_t* d_tdst, int32_t* d_scratch, void* stream);
-/* d_self_of: n_src int32 scratch                                        */
-int rg_sage_mean_bwd(const float* d_dself, const float* d_dmean, int64_t n_dst, int32_t H,
-                     const int32_t* d_cnt, const int32_t* d_self_pos, const int32_t* d_toff,
-                     const int32_t* d_tdst, int64_t n_src, int32_t* d_self_of, float* d_dh,
-                     void* stream);
+ * dmean[t] / max(cnt_t,1).  Dense [n, H] operands; d_self_of: n_src
+ * int32 scratch.                                                        */
+int rg_sage_mean_bwd(int32_t dtype, const void* d_dself, const void* d_dmean, int64_t n_dst,
+                     int32_t H, const int32_t* d_cnt, const int32_t* d_self_pos,
+                     const int32_t* d_toff, const int32_t* d_tdst, int64_t n_src,
+                     int32_t* d_self_of, void* d_dh, void* stream);
 
 /* ---- host-side graph materialisation (graph.py, partition.py) ------- */
 int rg_philox_raw(uint64_t key0, uint64_t key1, int64_t count, uint64_t* h_out);

@@ -19,7 +19,7 @@ INCLUDE = HERE.parent / "include"
 LIB = HERE / "librapidgnn_b200.so"
 STAMP = HERE / ".build_stamp"
 
-CU_SOURCES = ["rg_abi.cu", "rg_sampler.cu", "rg_gather.cu", "rg_gather_tma.cu", "rg_prefetch.cu",
+CU_SOURCES = ["rg_abi.cu", "rg_sampler.cu", "rg_gather.cu", "rg_prefetch.cu",
               "rg_plan.cu", "rg_sage.cu"]
 CPP_SOURCES = ["rg_host.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -71,7 +71,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         objs.append(obj)
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [nvcc, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs),
-           "-Xcompiler", "-fopenmp", "-lrt", "-ldl", "-lpthread"]
+           "-Xcompiler", "-fopenmp", "-Xlinker", f"--version-script={CSRC / 'rg_exports.map'}",
+           "-lrt", "-ldl", "-lpthread"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")

@@ -32,7 +32,7 @@ __global__ void probe_kernel(int* out) { *out = 100; }
 
 extern "C" const char* rg_last_error(void) { return rg::g_err; }
 
-extern "C" int rg_abi_version(void) { return 1; }
+extern "C" int rg_abi_version(void) { return 2; }
 
 extern "C" int rg_device_ok(void) {
   int dev = 0;

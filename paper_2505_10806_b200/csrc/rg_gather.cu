@@ -299,189 +299,6 @@ unsigned* queue_slot(cudaStream_t s) {
   return q;
 }
 
-// ---- staged peer rows (multi-GPU) ---------------------------------------
-// Rows of 400 B read at random over NVLink move as whole 128-B lines
-// (~600 GB/s payload cap, tools/nvlink_probe.py).  Owners therefore stage,
-// for every 32-row chunk of every batch slot, the rows they own into a
-// chunk-aligned buffer: stage[(b*cap + 32w + k)*stride], k = rank of the row
-// among the chunk's rows owned by that GPU.  A consumer computes the same k
-// from a ballot over owner ranks, so its peer reads are contiguous runs.
-struct StageInfo {
-  const float* stage[8];   // per rank (this rank's own entry unused)
-  uint8_t rank_of[16];     // partition -> rank
-  int my_rank;
-};
-
-// owner side: copy the rows this rank owns (any kind on this rank, cached or
-// not by the consumers) into the chunk-aligned staging buffer
-__global__ void __launch_bounds__(256)
-    stage_rows_kernel(const int32_t* __restrict__ ids, const int32_t* __restrict__ nids,
-                      int64_t cap, const uint32_t* __restrict__ base_route,
-                      const __grid_constant__ Bases bases, uint32_t mine_mask, int src_stride,
-                      int stride, int nvec, float* __restrict__ stage) {
-  __shared__ const float* s_base[16];
-  __shared__ unsigned long long s_src[8][32];
-  if (threadIdx.x < 16) s_base[threadIdx.x] = bases.p[threadIdx.x];
-  __syncthreads();
-  const int b = blockIdx.y;
-  const int lane = lane_id(), warp = threadIdx.x >> 5;
-  const unsigned lt = (1u << lane) - 1u;
-  const int nrows = nids[b];
-  const int64_t warp_stride = (int64_t)gridDim.x * 8 * 32;
-  for (int64_t r0 = ((int64_t)blockIdx.x * 8 + warp) * 32; r0 < nrows; r0 += warp_stride) {
-    const int64_t row = r0 + lane;
-    uint32_t rt = RG_ROUTE_INVALID;
-    if (row < nrows) rt = __ldg(base_route + __ldg(ids + (int64_t)b * cap + row));
-    const int kind = (int)(rt >> RG_KIND_SHIFT);
-    const bool mine = rt != RG_ROUTE_INVALID && ((mine_mask >> kind) & 1u);
-    const unsigned m = __ballot_sync(kFull, mine);
-    if (mine)  // the k-th owned row of the chunk -> staging slot k
-      s_src[warp][__popc(m & lt)] = reinterpret_cast<unsigned long long>(
-          s_base[kind] + (int64_t)(rt & RG_ROW_MASK) * src_stride);
-    __syncwarp();
-    const int total = __popc(m) * nvec;
-    float4* dst = reinterpret_cast<float4*>(stage + ((int64_t)b * cap + r0) * stride);
-    for (int e0 = 0; e0 < total; e0 += 32 * 4) {
-      float4 v[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int e = e0 + u * 32 + lane;
-        if (e < total) {
-          const int rr = e / nvec, c = e - rr * nvec;
-          v[u] = ld_stream(reinterpret_cast<const float4*>(s_src[warp][rr]) + c);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int e = e0 + u * 32 + lane;
-        if (e < total) st_stream(dst + e, v[u]);
-      }
-    }
-    __syncwarp();
-  }
-}
-
-// consumer side of the staged mode: as gather_bundle_kernel, but a row owned
-// by a partition on another rank is read from that rank's staging buffer at
-// its chunk-aligned slot (contiguous runs over NVLink).  Cache hits and this
-// rank's own partitions are read as usual.
-__global__ void __launch_bounds__(kGatherWarps * 32)
-    gather_staged_kernel(const int32_t* __restrict__ ids, const int32_t* __restrict__ nids,
-                         int64_t cap, const uint32_t* __restrict__ route,
-                         const uint8_t* __restrict__ owner, const __grid_constant__ Bases bases,
-                         const __grid_constant__ StageInfo si, int src_stride, int stride,
-                         int nvec, int dq, int dr, int my_part, uint32_t peer_mask,
-                         float* __restrict__ out, uint32_t* __restrict__ counters) {
-  __shared__ uint32_t s_cnt[RG_NCOUNTERS];
-  __shared__ const float* s_base[16];
-  __shared__ const float* s_stage[8];
-  __shared__ uint8_t s_rank[16];
-  const int b = blockIdx.y;
-  const int lane = lane_id();
-  const int warp = threadIdx.x >> 5;
-  const unsigned lt = (1u << lane) - 1u;
-  if (threadIdx.x < RG_NCOUNTERS) s_cnt[threadIdx.x] = 0;
-  if (threadIdx.x < 16) {
-    s_base[threadIdx.x] = bases.p[threadIdx.x];
-    s_rank[threadIdx.x] = si.rank_of[threadIdx.x];
-  }
-  if (threadIdx.x < 8) s_stage[threadIdx.x] = si.stage[threadIdx.x];
-  __syncthreads();
-  const int nrows = nids[b];
-  uint32_t c_local = 0, c_hit = 0, c_fb = 0, c_bad = 0, c_peer = 0, omask = 0;
-  const int64_t warp_stride = (int64_t)gridDim.x * kGatherWarps * 32;
-  for (int64_t r0 = ((int64_t)blockIdx.x * kGatherWarps + warp) * 32; r0 < nrows;
-       r0 += warp_stride) {
-    const int64_t row = r0 + lane;
-    const bool valid = row < nrows;
-    const int nr = (int)(nrows - r0 < 32 ? nrows - r0 : 32);
-    uint32_t rt = RG_ROUTE_INVALID;
-    int orank = -1;
-    if (valid) {
-      const int32_t id = __ldg(ids + (int64_t)b * cap + row);
-      rt = __ldg(route + id);
-      orank = s_rank[__ldg(owner + id) & 15];
-    }
-    // staging slot of this row inside its owner rank's chunk (computed for
-    // every rank present in the chunk; only peer rows use it)
-    int slot = 0;
-    for (int rk = 0; rk < 8; ++rk) {
-      const unsigned mr = __ballot_sync(kFull, orank == rk);
-      if (orank == rk) slot = __popc(mr & lt);
-    }
-    const int kind = (int)(rt >> RG_KIND_SHIFT);
-    const float* bp = (valid && rt != RG_ROUTE_INVALID) ? s_base[kind] : nullptr;
-    const bool bad = valid && bp == nullptr;
-    const bool local = valid && !bad && kind == my_part;
-    const bool hit = valid && !bad && kind == (int)RG_KIND_CACHE;
-    const bool fb = valid && !bad && !local && !hit;
-    const bool peer = fb && ((peer_mask >> kind) & 1u);
-    c_local += __popc(__ballot_sync(kFull, local));
-    c_hit += __popc(__ballot_sync(kFull, hit));
-    c_fb += __popc(__ballot_sync(kFull, fb));
-    c_bad += __popc(__ballot_sync(kFull, bad));
-    c_peer += __popc(__ballot_sync(kFull, peer));
-    omask |= __reduce_or_sync(kFull, fb ? (1u << kind) : 0u);
-    const float* src = nullptr;
-    if (peer)
-      src = s_stage[orank] + ((int64_t)b * cap + r0 + slot) * stride;
-    else if (bp)
-      src = bp + (int64_t)(rt & RG_ROW_MASK) * src_stride;
-    const unsigned long long srcu = reinterpret_cast<unsigned long long>(src);
-    float4* dst = reinterpret_cast<float4*>(out + ((int64_t)b * cap + r0) * stride);
-    const int total = nr * nvec;
-    int er = lane / nvec, ec = lane - (lane / nvec) * nvec;
-    for (int e0 = 0; e0 < total; e0 += 32 * kUnroll) {
-      float4 v[kUnroll];
-      int rr[kUnroll], cc[kUnroll];
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        rr[u] = er;
-        cc[u] = ec;
-        ec += dr;
-        er += dq;
-        if (ec >= nvec) {
-          ec -= nvec;
-          ++er;
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const unsigned long long sp = __shfl_sync(kFull, srcu, rr[u] & 31);
-        const int e = e0 + u * 32 + lane;
-        if (e < total && sp)
-          v[u] = ld_stream(reinterpret_cast<const float4*>(sp) + cc[u]);
-        else
-          v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const int e = e0 + u * 32 + lane;
-        if (e < total) st_stream(dst + e, v[u]);
-      }
-    }
-  }
-  if (lane == 0) {
-    atomicAdd(&s_cnt[RG_CNT_LOCAL], c_local);
-    atomicAdd(&s_cnt[RG_CNT_HIT], c_hit);
-    atomicAdd(&s_cnt[RG_CNT_FALLBACK], c_fb);
-    atomicAdd(&s_cnt[RG_CNT_BAD], c_bad);
-    atomicAdd(&s_cnt[RG_CNT_PEER], c_peer);
-    atomicOr(&s_cnt[RG_CNT_OWNER_MASK], omask);
-  }
-  __syncthreads();
-  if (threadIdx.x < RG_NCOUNTERS) {
-    const uint32_t x = s_cnt[threadIdx.x];
-    if (x) {
-      uint32_t* g = counters + (int64_t)b * RG_NCOUNTERS + threadIdx.x;
-      if (threadIdx.x == RG_CNT_OWNER_MASK)
-        atomicOr(g, x);
-      else
-        atomicAdd(g, x);
-    }
-  }
-}
-
 __global__ void route_copy_kernel(const uint32_t* __restrict__ base, int64_t n,
                                   uint32_t* __restrict__ route) {
   const int64_t n4 = n / 4;
@@ -587,55 +404,4 @@ extern "C" int rg_route_with_cache(const uint32_t* d_base_route, int64_t n, cons
   if (n_hot == 0) return RG_OK;
   route_scatter_kernel<<<kNumSMs * 2, 256, 0, s>>>(d_hot, n_hot, d_route);
   return check_launch("route_scatter");
-}
-
-extern "C" int rg_stage_rows(const int32_t* d_ids, const int32_t* d_nids, int64_t cap, int32_t G,
-                             const uint32_t* d_base_route, const float* const* h_bases,
-                             uint32_t mine_mask, int32_t src_stride, int32_t stride,
-                             float* d_stage, void* stream) {
-  RG_REQUIRE(G >= 1 && G <= 65535 && cap >= 1, "rg_stage_rows: bad sizes");
-  RG_REQUIRE(stride >= 4 && stride % 4 == 0 && src_stride >= stride && src_stride % 4 == 0,
-             "rg_stage_rows: bad strides");
-  Bases bases;
-  for (int i = 0; i < 16; ++i) bases.p[i] = h_bases[i];
-  const int64_t want = (cap + 255) / 256;
-  const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)kNumSMs * 4 / G));
-  stage_rows_kernel<<<dim3(gx, G), 256, 0, (cudaStream_t)stream>>>(
-      d_ids, d_nids, cap, d_base_route, bases, mine_mask, src_stride, stride, stride / 4,
-      d_stage);
-  return check_launch("stage_rows");
-}
-
-extern "C" int rg_gather_bundle_staged(const int32_t* d_ids, const int32_t* d_nids, int64_t cap,
-                                       int32_t G, const uint32_t* d_route,
-                                       const uint8_t* d_owner, const float* const* h_bases,
-                                       const float* const* h_stage, const uint8_t* h_rank_of,
-                                       int32_t my_rank, int32_t src_stride, int32_t stride,
-                                       int32_t my_part, uint32_t peer_mask, float* d_out,
-                                       uint32_t* d_counters, void* stream) {
-  RG_REQUIRE(G >= 1 && G <= 65535 && cap >= 1, "rg_gather_bundle_staged: bad sizes");
-  RG_REQUIRE(stride >= 4 && stride % 4 == 0 && src_stride >= stride && src_stride % 4 == 0,
-             "rg_gather_bundle_staged: bad strides");
-  Bases bases;
-  StageInfo si;
-  for (int i = 0; i < 16; ++i) {
-    bases.p[i] = h_bases[i];
-    si.rank_of[i] = h_rank_of[i];
-  }
-  for (int i = 0; i < 8; ++i) si.stage[i] = h_stage[i];
-  si.my_rank = my_rank;
-  const int nvec = stride / 4;
-  const int dq = 32 / nvec, dr = 32 % nvec;
-  static const int env_ctas = [] {
-    const char* e = getenv("RG_GATHER_CTAS_PER_SM");
-    return e ? std::max(1, atoi(e)) : 0;
-  }();
-  const int ctas_per_sm = env_ctas ? env_ctas : 6;
-  const int64_t want = (cap + kGatherWarps * 32 - 1) / (kGatherWarps * 32);
-  const int gx = (int)std::max<int64_t>(
-      1, std::min<int64_t>(want, ((int64_t)kNumSMs * ctas_per_sm) / G));
-  gather_staged_kernel<<<dim3(gx, G), kGatherWarps * 32, 0, (cudaStream_t)stream>>>(
-      d_ids, d_nids, cap, d_route, d_owner, bases, si, src_stride, stride, nvec, dq, dr, my_part,
-      peer_mask, d_out, d_counters);
-  return check_launch("gather_staged");
 }

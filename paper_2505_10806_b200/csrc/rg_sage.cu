@@ -3,13 +3,23 @@
 // Reference: gnnpipe/model.py:72-81 (_forward_pass) and model.py:126-135
 // (loss_and_grad backward scatter).  The reference sums neighbour rows with
 // np.add.at in edge order (dst asc, src asc), divides by max(count, 1) in
-// fp32, and in the backward adds dself at the self positions first and then
-// (dmean / denom)[dst] into dh[src] in the same edge order.  Both kernels
-// reproduce those orders exactly (one sequential fp32 chain per output
-// element, parallel over columns), so results are bit-identical to the
-// reference for identical inputs; only the dense GEMMs around them (cuBLAS)
-// differ in rounding.
+// the parameter dtype, and in the backward adds dself at the self positions
+// first and then (dmean / denom)[dst] into dh[src] in the same edge order.
+// Both kernels reproduce those orders exactly (one sequential chain per
+// output element, parallel over columns), so results are bit-identical to
+// the reference for identical inputs in fp32 and fp64 (RunConfig.precision,
+// train.py:117); only the dense GEMMs around them (cuBLAS) differ in rounding.
+//
+// Positions (model.py:53-55, 74-75: searchsorted of src / dst into the
+// sorted src frontier) are resolved ONCE per level by rg_sage_positions —
+// a scatter of frontier ranks into an n-node rank table, then one load per
+// edge — and shared by the forward and the backward.  The backward's
+// transposed index (edges grouped by src, ascending dst inside a group =
+// the reference's edge order for that src) is a stable radix sort of the
+// edges by src position, so any in-sample in-degree is handled exactly.
 #include <climits>
+
+#include <cub/device/device_radix_sort.cuh>
 
 #include "rg_common.cuh"
 
@@ -17,198 +27,134 @@ namespace rg {
 namespace {
 
 constexpr int kWarps = 8;
-constexpr int kSortCap = 4096;
 
-__device__ __forceinline__ int lower_bound(const int32_t* __restrict__ a, int64_t n, int32_t x) {
-  int64_t lo = 0, hi = n;
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (__ldg(a + mid) < x)
-      lo = mid + 1;
-    else
-      hi = mid;
-  }
-  return (int)lo;
+// ---------------------------------------------------------------- positions
+__global__ void rank_scatter_kernel(const int32_t* __restrict__ front, int64_t n,
+                                    int32_t* __restrict__ rank) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x)
+    rank[front[j]] = (int32_t)j;
 }
 
-// warp per destination row t; columns strided over lanes, 4 per lane per tile
+// epos[t*F + r] = rank of ell[t*F + r] (r < cnt[t]), -1 past the row's count;
+// self_pos[t] = rank of dst_front[t] (frontiers are nested: dst ⊂ src)
+__global__ void edge_pos_kernel(const int32_t* __restrict__ rank,
+                                const int32_t* __restrict__ dst_front, int64_t n_dst,
+                                const int32_t* __restrict__ ell, const int32_t* __restrict__ cnt,
+                                int F, int32_t* __restrict__ epos,
+                                int32_t* __restrict__ self_pos) {
+  const int64_t total = n_dst * F;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = i / F;
+    const int r = (int)(i - t * F);
+    epos[i] = r < __ldg(cnt + t) ? __ldg(rank + __ldg(ell + i)) : -1;
+    if (r == 0) self_pos[t] = __ldg(rank + __ldg(dst_front + t));
+  }
+}
+
+// ---------------------------------------------------------------- row tiles
+// N elements of T moved as one aligned load (16 B for float4 / double2)
+template <typename T, int N>
+struct alignas(sizeof(T) * N) Vec {
+  T v[N];
+};
+
+// A group of SW lanes owns one output row; lane j of the group handles the
+// row's vectors j, j + SW, ... (up to kVPL per pass over the columns).
+constexpr int kVPL = 4;
+
+template <typename T, int N>
+__device__ __forceinline__ void load_vecs(const T* __restrict__ row, int nvec, int j0, int SW,
+                                          Vec<T, N> (&x)[kVPL]) {
+#pragma unroll
+  for (int u = 0; u < kVPL; ++u) {
+    const int vi = j0 + u * SW;
+    if (vi < nvec) x[u] = *reinterpret_cast<const Vec<T, N>*>(row + (int64_t)vi * N);
+  }
+}
+
+// mean[t] = (((0 + h[p_1]) + h[p_2]) + ...) / max(cnt_t, 1); self[t] = h[self_pos[t]]
+template <typename T, int N>
 __global__ void __launch_bounds__(kWarps * 32)
-    sage_fwd_kernel(const float* __restrict__ h, int64_t n_src, int H, int ldh,
-                    const int32_t* __restrict__ src_front, const int32_t* __restrict__ dst_front,
-                    int64_t n_dst, const int32_t* __restrict__ ell, const int32_t* __restrict__ cnt,
-                    int F, float* __restrict__ mean, float* __restrict__ self,
-                    int32_t* __restrict__ self_pos) {
+    sage_fwd_kernel(const T* __restrict__ h, int ldh, int H, const int32_t* __restrict__ epos,
+                    const int32_t* __restrict__ self_pos, int64_t n_dst,
+                    const int32_t* __restrict__ cnt, int F, int SW, T* __restrict__ mean,
+                    T* __restrict__ self) {
   const int lane = lane_id();
-  const int64_t nw = (int64_t)gridDim.x * kWarps;
-  for (int64_t t = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); t < n_dst; t += nw) {
-    const int c = cnt[t];
-    const float denom = (float)max(c, 1);
-    const int ps = lower_bound(src_front, n_src, dst_front[t]);
-    if (lane == 0 && self_pos) self_pos[t] = ps;
-    int p_lane = 0;
-    if (lane < c) p_lane = lower_bound(src_front, n_src, ell[t * F + lane]);
-    for (int col0 = 0; col0 < H; col0 += 128) {
-      float acc[4] = {0.f, 0.f, 0.f, 0.f};
-      for (int r0 = 0; r0 < c; r0 += 32) {
-        int p_chunk = p_lane;
-        if (r0 > 0) {
-          const int r = r0 + lane;
-          p_chunk = r < c ? lower_bound(src_front, n_src, ell[t * F + r]) : 0;
-        }
-        const int nr = min(32, c - r0);
-        for (int rr = 0; rr < nr; ++rr) {
-          const int p = __shfl_sync(kFull, p_chunk, rr);
-          const float* hp = h + (int64_t)p * ldh;
+  const int rpw = 32 / SW;  // rows per warp
+  const int grp = lane / SW, j0 = lane % SW;
+  const int nvec = H / N;
+  const int64_t nrow_step = (int64_t)gridDim.x * kWarps * rpw;
+  for (int64_t t = ((int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5)) * rpw + grp; t < n_dst;
+       t += nrow_step) {
+    const int c = __ldg(cnt + t);
+    const T denom = (T)max(c, 1);
+    const int32_t* ep = epos + t * F;
+    const int ps = __ldg(self_pos + t);
+    for (int vb = 0; vb < nvec; vb += SW * kVPL) {
+      const int jb = vb + j0;
+      Vec<T, N> acc[kVPL];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int col = col0 + u * 32 + lane;
-            if (col < H) acc[u] += __ldg(hp + col);
-          }
-        }
+      for (int u = 0; u < kVPL; ++u)
+#pragma unroll
+        for (int k = 0; k < N; ++k) acc[u].v[k] = (T)0;
+      int r = 0;
+      for (; r + 2 <= c; r += 2) {  // two rows' loads in flight, adds in edge order
+        Vec<T, N> x0[kVPL], x1[kVPL];
+        load_vecs<T, N>(h + (int64_t)__ldg(ep + r) * ldh, nvec, jb, SW, x0);
+        load_vecs<T, N>(h + (int64_t)__ldg(ep + r + 1) * ldh, nvec, jb, SW, x1);
+#pragma unroll
+        for (int u = 0; u < kVPL; ++u)
+#pragma unroll
+          for (int k = 0; k < N; ++k) acc[u].v[k] = (acc[u].v[k] + x0[u].v[k]) + x1[u].v[k];
       }
+      if (r < c) {
+        Vec<T, N> x0[kVPL];
+        load_vecs<T, N>(h + (int64_t)__ldg(ep + r) * ldh, nvec, jb, SW, x0);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int col = col0 + u * 32 + lane;
-        if (col < H) {
-          mean[t * H + col] = acc[u] / denom;
-          if (self) self[t * H + col] = __ldg(h + (int64_t)ps * ldh + col);
+        for (int u = 0; u < kVPL; ++u)
+#pragma unroll
+          for (int k = 0; k < N; ++k) acc[u].v[k] += x0[u].v[k];
+      }
+      Vec<T, N> sv[kVPL];
+      if (self) load_vecs<T, N>(h + (int64_t)ps * ldh, nvec, jb, SW, sv);
+#pragma unroll
+      for (int u = 0; u < kVPL; ++u) {
+        const int vi = jb + u * SW;
+        if (vi < nvec) {
+#pragma unroll
+          for (int k = 0; k < N; ++k) acc[u].v[k] = acc[u].v[k] / denom;
+          *reinterpret_cast<Vec<T, N>*>(mean + t * H + (int64_t)vi * N) = acc[u];
+          if (self) *reinterpret_cast<Vec<T, N>*>(self + t * H + (int64_t)vi * N) = sv[u];
         }
       }
     }
   }
 }
 
-// edge -> src position (ELL aligned) and per-src in-degree
-__global__ void transpose_count_kernel(const int32_t* __restrict__ src_front, int64_t n_src,
-                                       const int32_t* __restrict__ ell,
-                                       const int32_t* __restrict__ cnt, int64_t n_dst, int F,
-                                       int32_t* __restrict__ epos, int32_t* __restrict__ deg) {
-  const int64_t total = n_dst * F;
+// ---------------------------------------------------------------- transpose
+// toff[s] = first sorted index with key >= s (keys ascending, sentinel n_src)
+__global__ void segment_bounds_kernel(const int32_t* __restrict__ keys, int64_t nkeys,
+                                      int64_t n_src, int32_t* __restrict__ toff) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= nkeys;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = i < nkeys ? (int64_t)keys[i] : n_src;
+    const int64_t kp = i > 0 ? (int64_t)keys[i - 1] : -1;
+    for (int64_t s = kp + 1; s <= min(k, n_src); ++s) toff[s] = (int32_t)i;
+  }
+}
+
+// radix-sort input: key = src position (holes -> n_src, sorted last),
+// value = dst row; input order is the reference's edge order (t asc, r asc)
+__global__ void transpose_keys_kernel(const int32_t* __restrict__ epos, int64_t total, int F,
+                                      int32_t n_src, int32_t* __restrict__ keys,
+                                      int32_t* __restrict__ vals) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t t = i / F;
-    const int r = (int)(i - t * F);
-    if (r < cnt[t]) {
-      const int p = lower_bound(src_front, n_src, ell[i]);
-      epos[i] = p;
-      atomicAdd(deg + p, 1);
-    }
-  }
-}
-
-// exclusive scan of deg[0..n) into off[0..n], single pass per 1024-chunk
-// with the chunk base taken from a preceding count pass (two kernels).
-constexpr int kScanChunk = 1024;
-__global__ void __launch_bounds__(256)
-    chunk_sum_kernel(const int32_t* __restrict__ x, int64_t n, int32_t* __restrict__ tot) {
-  __shared__ int s_red[32];
-  const int64_t i0 = (int64_t)blockIdx.x * kScanChunk + threadIdx.x * 4;
-  int c = 0;
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-    if (i0 + i < n) c += x[i0 + i];
-  int total;
-  block_excl_scan<256>(c, s_red, &total);
-  if (threadIdx.x == 0) tot[blockIdx.x] = total;
-}
-
-__global__ void __launch_bounds__(256)
-    chunk_scan_kernel(const int32_t* __restrict__ x, int64_t n, const int32_t* __restrict__ tot,
-                      int64_t nchunks, int32_t* __restrict__ off) {
-  __shared__ int s_red[32];
-  __shared__ int s_base;
-  int before = 0, all = 0;
-  for (int64_t c = threadIdx.x; c < nchunks; c += blockDim.x) {
-    all += tot[c];
-    if (c < (int64_t)blockIdx.x) before += tot[c];
-  }
-  int t;
-  block_excl_scan<256>(before, s_red, &t);
-  if (threadIdx.x == 0) s_base = t;
-  __syncthreads();
-  const int base = s_base;
-  __syncthreads();
-  int grand;
-  block_excl_scan<256>(all, s_red, &grand);
-  if (blockIdx.x == 0 && threadIdx.x == 0) off[n] = grand;
-  const int64_t i0 = (int64_t)blockIdx.x * kScanChunk + threadIdx.x * 4;
-  int v[4], s = 0;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    v[i] = i0 + i < n ? x[i0 + i] : 0;
-    s += v[i];
-  }
-  int dummy;
-  int at = base + block_excl_scan<256>(s, s_red, &dummy);
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    if (i0 + i < n) off[i0 + i] = at;
-    at += v[i];
-  }
-}
-
-__global__ void transpose_fill_kernel(const int32_t* __restrict__ cnt, int64_t n_dst, int F,
-                                      const int32_t* __restrict__ epos,
-                                      const int32_t* __restrict__ toff, int32_t* __restrict__ fill,
-                                      int32_t* __restrict__ tdst) {
-  const int64_t total = n_dst * F;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t t = i / F;
-    const int r = (int)(i - t * F);
-    if (r < cnt[t]) {
-      const int p = epos[i];
-      tdst[toff[p] + atomicAdd(fill + p, 1)] = (int32_t)t;
-    }
-  }
-}
-
-// sort every src segment of tdst ascending (restores the reference's edge
-// order for each src); warp per segment up to 32, CTA + smem beyond.
-__global__ void __launch_bounds__(256)
-    segment_sort_kernel(const int32_t* __restrict__ toff, int64_t n_src,
-                        int32_t* __restrict__ tdst, int32_t* __restrict__ err) {
-  __shared__ int32_t s_val[kSortCap];
-  const int lane = lane_id();
-  const int warp = threadIdx.x >> 5;
-  const int64_t nw = (int64_t)gridDim.x * 8;
-  for (int64_t s = (int64_t)blockIdx.x * 8 + warp; s < n_src; s += nw) {
-    const int a = toff[s], len = toff[s + 1] - a;
-    if (len <= 1 || len > 32) continue;
-    int32_t x = lane < len ? tdst[a + lane] : INT_MAX;
-    warp_bitonic_sort_keys(x);
-    if (lane < len) tdst[a + lane] = x;
-  }
-  // long segments: whole CTA, one at a time
-  for (int64_t s = blockIdx.x; s < n_src; s += gridDim.x) {
-    const int a = toff[s], len = toff[s + 1] - a;
-    if (len <= 32) continue;
-    if (len > kSortCap) {
-      if (threadIdx.x == 0) atomicExch(err, 1);
-      continue;
-    }
-    int P = 1;
-    while (P < len) P <<= 1;
-    for (int i = threadIdx.x; i < P; i += blockDim.x) s_val[i] = i < len ? tdst[a + i] : INT_MAX;
-    __syncthreads();
-    for (int k = 2; k <= P; k <<= 1) {
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        for (int i = threadIdx.x; i < P; i += blockDim.x) {
-          const int l = i ^ j;
-          if (l > i) {
-            const bool up = (i & k) == 0;
-            const int32_t x = s_val[i], y = s_val[l];
-            if ((x > y) == up) {
-              s_val[i] = y;
-              s_val[l] = x;
-            }
-          }
-        }
-        __syncthreads();
-      }
-    }
-    for (int i = threadIdx.x; i < len; i += blockDim.x) tdst[a + i] = s_val[i];
-    __syncthreads();
+    const int32_t p = epos[i];
+    keys[i] = p >= 0 ? p : n_src;
+    vals[i] = (int32_t)(i / F);
   }
 }
 
@@ -219,41 +165,127 @@ __global__ void self_of_kernel(const int32_t* __restrict__ self_pos, int64_t n_d
     self_of[self_pos[t]] = (int32_t)t;
 }
 
+// dh[s] = ((0 + dself[self_of[s]]) + dmean[t_1]/denom_1) + dmean[t_2]/denom_2 ...
+template <typename T, int N>
 __global__ void __launch_bounds__(kWarps * 32)
-    sage_bwd_kernel(const float* __restrict__ dself, const float* __restrict__ dmean, int H,
+    sage_bwd_kernel(const T* __restrict__ dself, const T* __restrict__ dmean, int H,
                     const int32_t* __restrict__ cnt, const int32_t* __restrict__ self_of,
                     const int32_t* __restrict__ toff, const int32_t* __restrict__ tdst,
-                    int64_t n_src, float* __restrict__ dh) {
+                    int64_t n_src, int SW, T* __restrict__ dh) {
   const int lane = lane_id();
-  const int64_t nw = (int64_t)gridDim.x * kWarps;
-  for (int64_t s = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); s < n_src; s += nw) {
-    const int a = toff[s], len = toff[s + 1] - a;
-    const int so = self_of[s];
-    for (int col0 = 0; col0 < H; col0 += 128) {
-      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  const int rpw = 32 / SW;
+  const int grp = lane / SW, j0 = lane % SW;
+  const int nvec = H / N;
+  const int64_t nrow_step = (int64_t)gridDim.x * kWarps * rpw;
+  for (int64_t s = ((int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5)) * rpw + grp; s < n_src;
+       s += nrow_step) {
+    const int a = __ldg(toff + s), len = __ldg(toff + s + 1) - a;
+    const int so = __ldg(self_of + s);
+    for (int vb = 0; vb < nvec; vb += SW * kVPL) {
+      const int jb = vb + j0;
+      Vec<T, N> acc[kVPL];
+#pragma unroll
+      for (int u = 0; u < kVPL; ++u)
+#pragma unroll
+        for (int k = 0; k < N; ++k) acc[u].v[k] = (T)0;
       if (so >= 0) {
+        Vec<T, N> x[kVPL];
+        load_vecs<T, N>(dself + (int64_t)so * H, nvec, jb, SW, x);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int col = col0 + u * 32 + lane;
-          if (col < H) acc[u] += dself[(int64_t)so * H + col];
-        }
+        for (int u = 0; u < kVPL; ++u)
+#pragma unroll
+          for (int k = 0; k < N; ++k) acc[u].v[k] += x[u].v[k];
       }
-      for (int k = 0; k < len; ++k) {
-        const int t = __ldg(tdst + a + k);
-        const float denom = (float)max(__ldg(cnt + t), 1);
+      int q = 0;
+      for (; q + 2 <= len; q += 2) {
+        const int t0 = __ldg(tdst + a + q), t1 = __ldg(tdst + a + q + 1);
+        const T d0 = (T)max(__ldg(cnt + t0), 1), d1 = (T)max(__ldg(cnt + t1), 1);
+        Vec<T, N> x0[kVPL], x1[kVPL];
+        load_vecs<T, N>(dmean + (int64_t)t0 * H, nvec, jb, SW, x0);
+        load_vecs<T, N>(dmean + (int64_t)t1 * H, nvec, jb, SW, x1);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int col = col0 + u * 32 + lane;
-          if (col < H) acc[u] += __ldg(dmean + (int64_t)t * H + col) / denom;
-        }
+        for (int u = 0; u < kVPL; ++u)
+#pragma unroll
+          for (int k = 0; k < N; ++k)
+            acc[u].v[k] = (acc[u].v[k] + x0[u].v[k] / d0) + x1[u].v[k] / d1;
+      }
+      if (q < len) {
+        const int t0 = __ldg(tdst + a + q);
+        const T d0 = (T)max(__ldg(cnt + t0), 1);
+        Vec<T, N> x0[kVPL];
+        load_vecs<T, N>(dmean + (int64_t)t0 * H, nvec, jb, SW, x0);
+#pragma unroll
+        for (int u = 0; u < kVPL; ++u)
+#pragma unroll
+          for (int k = 0; k < N; ++k) acc[u].v[k] += x0[u].v[k] / d0;
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int col = col0 + u * 32 + lane;
-        if (col < H) dh[s * H + col] = acc[u];
+      for (int u = 0; u < kVPL; ++u) {
+        const int vi = jb + u * SW;
+        if (vi < nvec) *reinterpret_cast<Vec<T, N>*>(dh + s * H + (int64_t)vi * N) = acc[u];
       }
     }
   }
+}
+
+// widest vector (<= 16 B) that divides H and the row pitch and keeps the
+// base pointers aligned
+template <typename T>
+int vec_width(int H, int64_t pitch, std::initializer_list<const void*> ptrs) {
+  for (int n = 16 / (int)sizeof(T); n > 1; n >>= 1) {
+    bool ok = H % n == 0 && pitch % n == 0;
+    for (const void* p : ptrs)
+      if (p && (reinterpret_cast<uintptr_t>(p) % (n * sizeof(T))) != 0) ok = false;
+    if (ok) return n;
+  }
+  return 1;
+}
+
+int sub_warp(int nvec) {
+  int sw = 1;
+  while (sw < 32 && sw < nvec) sw <<= 1;
+  return sw;
+}
+
+template <typename T, int N>
+int launch_fwd(const void* h, int ldh, int H, const int32_t* epos, const int32_t* self_pos,
+               int64_t n_dst, const int32_t* cnt, int F, void* mean, void* self,
+               cudaStream_t s) {
+  const int SW = sub_warp(H / N);
+  const int64_t rows_per_cta = (int64_t)kWarps * (32 / SW);
+  const int grid = (int)std::min<int64_t>((n_dst + rows_per_cta - 1) / rows_per_cta, kNumSMs * 16);
+  sage_fwd_kernel<T, N><<<grid, kWarps * 32, 0, s>>>(
+      (const T*)h, ldh, H, epos, self_pos, n_dst, cnt, F, SW, (T*)mean, (T*)self);
+  return check_launch("sage_fwd");
+}
+
+template <typename T, int N>
+int launch_bwd(const void* dself, const void* dmean, int H, const int32_t* cnt,
+               const int32_t* self_of, const int32_t* toff, const int32_t* tdst, int64_t n_src,
+               void* dh, cudaStream_t s) {
+  const int SW = sub_warp(H / N);
+  const int64_t rows_per_cta = (int64_t)kWarps * (32 / SW);
+  const int grid = (int)std::min<int64_t>((n_src + rows_per_cta - 1) / rows_per_cta, kNumSMs * 16);
+  sage_bwd_kernel<T, N><<<grid, kWarps * 32, 0, s>>>((const T*)dself, (const T*)dmean, H, cnt,
+                                                     self_of, toff, tdst, n_src, SW, (T*)dh);
+  return check_launch("sage_bwd");
+}
+
+constexpr size_t kAlign = 256;
+size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+size_t cub_temp_bytes(int64_t nitems, int end_bit) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const int32_t*)nullptr, (int32_t*)nullptr,
+                                  (const int32_t*)nullptr, (int32_t*)nullptr, (int)nitems, 0,
+                                  end_bit);
+  return bytes;
+}
+
+int key_bits(int64_t n_src) {
+  int b = 1;
+  while (b < 31 && (int64_t(1) << b) <= n_src) ++b;
+  return b;
 }
 
 }  // namespace
@@ -261,60 +293,95 @@ __global__ void __launch_bounds__(kWarps * 32)
 
 using namespace rg;
 
-extern "C" int rg_sage_mean_fwd(const float* d_h, int64_t n_src, int32_t H, int32_t ldh,
-                                const int32_t* d_src_front, const int32_t* d_dst_front,
-                                int64_t n_dst, const int32_t* d_ell, const int32_t* d_cnt,
-                                int32_t fanout, float* d_mean, float* d_self, int32_t* d_self_pos,
-                                void* stream) {
-  RG_REQUIRE(H >= 1 && ldh >= H && n_src >= 1 && n_dst >= 0 && fanout >= 1,
-             "rg_sage_mean_fwd: bad sizes");
+extern "C" int rg_sage_positions(const int32_t* d_src_front, int64_t n_src,
+                                 const int32_t* d_dst_front, int64_t n_dst, const int32_t* d_ell,
+                                 const int32_t* d_cnt, int32_t fanout, int64_t n_nodes,
+                                 int32_t* d_rank, int32_t* d_epos, int32_t* d_self_pos,
+                                 void* stream) {
+  RG_REQUIRE(n_src >= 1 && n_src <= INT32_MAX && n_dst >= 0 && fanout >= 1 && n_nodes >= n_src,
+             "rg_sage_positions: bad sizes");
+  RG_REQUIRE(n_dst * (int64_t)fanout < INT32_MAX, "rg_sage_positions: n_dst * fanout overflows");
   if (n_dst == 0) return RG_OK;
-  const int grid = (int)std::min<int64_t>((n_dst + kWarps - 1) / kWarps, kNumSMs * 16);
-  sage_fwd_kernel<<<grid, kWarps * 32, 0, (cudaStream_t)stream>>>(
-      d_h, n_src, H, ldh, d_src_front, d_dst_front, n_dst, d_ell, d_cnt, fanout, d_mean, d_self,
-      d_self_pos);
-  return check_launch("sage_fwd");
+  cudaStream_t s = (cudaStream_t)stream;
+  rank_scatter_kernel<<<(unsigned)std::min<int64_t>((n_src + 255) / 256, kNumSMs * 8), 256, 0, s>>>(
+      d_src_front, n_src, d_rank);
+  int rc = check_launch("rank_scatter");
+  if (rc) return rc;
+  const int64_t total = n_dst * fanout;
+  edge_pos_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, kNumSMs * 8), 256, 0, s>>>(
+      d_rank, d_dst_front, n_dst, d_ell, d_cnt, fanout, d_epos, d_self_pos);
+  return check_launch("edge_pos");
 }
 
-extern "C" int rg_sage_transpose(const int32_t* d_src_front, int64_t n_src, const int32_t* d_ell,
-                                 const int32_t* d_cnt, int64_t n_dst, int32_t fanout,
-                                 int32_t* d_toff, int32_t* d_tdst, int32_t* d_scratch,
-                                 void* stream) {
-  RG_REQUIRE(n_src >= 1 && n_dst >= 0 && fanout >= 1, "rg_sage_transpose: bad sizes");
+extern "C" int rg_sage_mean_fwd(int32_t dtype, const void* d_h, int32_t H, int32_t ldh,
+                                const int32_t* d_epos, const int32_t* d_self_pos, int64_t n_dst,
+                                const int32_t* d_cnt, int32_t fanout, void* d_mean, void* d_self,
+                                void* stream) {
+  RG_REQUIRE(H >= 1 && ldh >= H && n_dst >= 0 && fanout >= 1, "rg_sage_mean_fwd: bad sizes");
+  RG_REQUIRE(dtype == RG_DTYPE_F32 || dtype == RG_DTYPE_F64, "rg_sage_mean_fwd: bad dtype");
+  if (n_dst == 0) return RG_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  // scratch layout: deg[n_src] | fill[n_src] | err[1] | chunk[nchunks] | epos[n_dst*F]
-  const int64_t nchunks = (n_src + kScanChunk - 1) / kScanChunk;
-  int32_t* deg = d_scratch;
-  int32_t* fill = deg + n_src;
-  int32_t* err = fill + n_src;
-  int32_t* chunk = err + 1;
-  int32_t* epos = chunk + nchunks;
-  if (cudaMemsetAsync(deg, 0, sizeof(int32_t) * (2 * n_src + 1), s) != cudaSuccess)
-    return check_launch("transpose memset");
-  const int g = kNumSMs * 8;
-  transpose_count_kernel<<<g, 256, 0, s>>>(d_src_front, n_src, d_ell, d_cnt, n_dst, fanout, epos,
-                                           deg);
-  int rc = check_launch("transpose_count");
-  if (rc) return rc;
-  chunk_sum_kernel<<<(unsigned)nchunks, 256, 0, s>>>(deg, n_src, chunk);
-  if ((rc = check_launch("chunk_sum"))) return rc;
-  chunk_scan_kernel<<<(unsigned)nchunks, 256, 0, s>>>(deg, n_src, chunk, nchunks, d_toff);
-  if ((rc = check_launch("chunk_scan"))) return rc;
-  transpose_fill_kernel<<<g, 256, 0, s>>>(d_cnt, n_dst, fanout, epos, d_toff, fill, d_tdst);
-  if ((rc = check_launch("transpose_fill"))) return rc;
-  segment_sort_kernel<<<kNumSMs * 2, 256, 0, s>>>(d_toff, n_src, d_tdst, err);
-  return check_launch("segment_sort");
+  if (dtype == RG_DTYPE_F32) {
+    switch (vec_width<float>(H, ldh, {d_h, d_mean, d_self})) {
+      case 4: return launch_fwd<float, 4>(d_h, ldh, H, d_epos, d_self_pos, n_dst, d_cnt, fanout, d_mean, d_self, s);
+      case 2: return launch_fwd<float, 2>(d_h, ldh, H, d_epos, d_self_pos, n_dst, d_cnt, fanout, d_mean, d_self, s);
+      default: return launch_fwd<float, 1>(d_h, ldh, H, d_epos, d_self_pos, n_dst, d_cnt, fanout, d_mean, d_self, s);
+    }
+  }
+  if (vec_width<double>(H, ldh, {d_h, d_mean, d_self}) == 2)
+    return launch_fwd<double, 2>(d_h, ldh, H, d_epos, d_self_pos, n_dst, d_cnt, fanout, d_mean, d_self, s);
+  return launch_fwd<double, 1>(d_h, ldh, H, d_epos, d_self_pos, n_dst, d_cnt, fanout, d_mean, d_self, s);
 }
 
 extern "C" int64_t rg_sage_transpose_scratch(int64_t n_src, int64_t n_dst, int32_t fanout) {
-  return 2 * n_src + 1 + (n_src + kScanChunk - 1) / kScanChunk + n_dst * fanout;
+  const int64_t total = n_dst * fanout;
+  if (n_src < 1 || total < 0 || total >= INT32_MAX) return -1;
+  return (int64_t)(3 * align_up(sizeof(int32_t) * std::max<int64_t>(total, 1)) +
+                   align_up(cub_temp_bytes(total, key_bits(n_src))));
 }
 
-extern "C" int rg_sage_mean_bwd(const float* d_dself, const float* d_dmean, int64_t n_dst,
-                                int32_t H, const int32_t* d_cnt, const int32_t* d_self_pos,
-                                const int32_t* d_toff, const int32_t* d_tdst, int64_t n_src,
-                                int32_t* d_self_of, float* d_dh, void* stream) {
+extern "C" int rg_sage_transpose(const int32_t* d_epos, const int32_t* d_cnt, int64_t n_dst,
+                                 int32_t fanout, int64_t n_src, int32_t* d_toff, int32_t* d_tdst,
+                                 void* d_scratch, int64_t scratch_bytes, void* stream) {
+  (void)d_cnt;
+  RG_REQUIRE(n_src >= 1 && n_src < INT32_MAX && n_dst >= 0 && fanout >= 1,
+             "rg_sage_transpose: bad sizes");
+  const int64_t need = rg_sage_transpose_scratch(n_src, n_dst, fanout);
+  RG_REQUIRE(need >= 0 && scratch_bytes >= need, "rg_sage_transpose: scratch %lld < %lld bytes",
+             (long long)scratch_bytes, (long long)need);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t total = n_dst * fanout;
+  char* base = (char*)d_scratch;
+  const size_t arr = align_up(sizeof(int32_t) * std::max<int64_t>(total, 1));
+  int32_t* keys_in = (int32_t*)base;
+  int32_t* vals_in = (int32_t*)(base + arr);
+  int32_t* keys_out = (int32_t*)(base + 2 * arr);
+  void* temp = base + 3 * arr;
+  int rc;
+  if (total > 0) {
+    const unsigned g = (unsigned)std::min<int64_t>((total + 255) / 256, kNumSMs * 8);
+    transpose_keys_kernel<<<g, 256, 0, s>>>(d_epos, total, fanout, (int32_t)n_src, keys_in,
+                                            vals_in);
+    if ((rc = check_launch("transpose_keys"))) return rc;
+    const int bits = key_bits(n_src);
+    size_t temp_bytes = cub_temp_bytes(total, bits);
+    // stable LSD radix sort: per src the dst rows keep their edge order
+    if (cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, vals_in, d_tdst,
+                                        (int)total, 0, bits, s) != cudaSuccess)
+      return check_launch("transpose radix sort");
+  }
+  const unsigned g = (unsigned)std::min<int64_t>((total + 1 + 255) / 256, kNumSMs * 8);
+  segment_bounds_kernel<<<g, 256, 0, s>>>(keys_out, total, n_src, d_toff);
+  return check_launch("segment_bounds");
+}
+
+extern "C" int rg_sage_mean_bwd(int32_t dtype, const void* d_dself, const void* d_dmean,
+                                int64_t n_dst, int32_t H, const int32_t* d_cnt,
+                                const int32_t* d_self_pos, const int32_t* d_toff,
+                                const int32_t* d_tdst, int64_t n_src, int32_t* d_self_of,
+                                void* d_dh, void* stream) {
   RG_REQUIRE(H >= 1 && n_src >= 1 && n_dst >= 0, "rg_sage_mean_bwd: bad sizes");
+  RG_REQUIRE(dtype == RG_DTYPE_F32 || dtype == RG_DTYPE_F64, "rg_sage_mean_bwd: bad dtype");
   cudaStream_t s = (cudaStream_t)stream;
   if (cudaMemsetAsync(d_self_of, 0xff, sizeof(int32_t) * n_src, s) != cudaSuccess)
     return check_launch("bwd memset");
@@ -323,8 +390,14 @@ extern "C" int rg_sage_mean_bwd(const float* d_dself, const float* d_dmean, int6
     int rc = check_launch("self_of");
     if (rc) return rc;
   }
-  const int grid = (int)std::min<int64_t>((n_src + kWarps - 1) / kWarps, kNumSMs * 16);
-  sage_bwd_kernel<<<grid, kWarps * 32, 0, s>>>(d_dself, d_dmean, H, d_cnt, d_self_of, d_toff,
-                                               d_tdst, n_src, d_dh);
-  return check_launch("sage_bwd");
+  if (dtype == RG_DTYPE_F32) {
+    switch (vec_width<float>(H, H, {d_dself, d_dmean, d_dh})) {
+      case 4: return launch_bwd<float, 4>(d_dself, d_dmean, H, d_cnt, d_self_of, d_toff, d_tdst, n_src, d_dh, s);
+      case 2: return launch_bwd<float, 2>(d_dself, d_dmean, H, d_cnt, d_self_of, d_toff, d_tdst, n_src, d_dh, s);
+      default: return launch_bwd<float, 1>(d_dself, d_dmean, H, d_cnt, d_self_of, d_toff, d_tdst, n_src, d_dh, s);
+    }
+  }
+  if (vec_width<double>(H, H, {d_dself, d_dmean, d_dh}) == 2)
+    return launch_bwd<double, 2>(d_dself, d_dmean, H, d_cnt, d_self_of, d_toff, d_tdst, n_src, d_dh, s);
+  return launch_bwd<double, 1>(d_dself, d_dmean, H, d_cnt, d_self_of, d_toff, d_tdst, n_src, d_dh, s);
 }

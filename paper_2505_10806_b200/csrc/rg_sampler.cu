@@ -555,7 +555,7 @@ __global__ void __launch_bounds__(256)
   __shared__ int s_rank, s_fill;
   const int nslow = slow[0];
   for (int it = blockIdx.x; it < nslow; it += gridDim.x) {
-    const int64_t k = slow[1 + it];
+    const int64_t k = (uint32_t)slow[1 + it];  // queue items are < 2^32 (host check)
     const int j = (int)(k / G), b = (int)(k - (int64_t)j * G);
     const int64_t row = (int64_t)b * cap_in + j;
     const int32_t v = front[row];
@@ -565,9 +565,13 @@ __global__ void __launch_bounds__(256)
     if (D <= F) {
       for (int p = threadIdx.x; p < D; p += blockDim.x) s_val[p] = indices[a + p];
     } else if (prng != kSplitMix) {
-      // Floyd over a D-bit membership bitmap (D <= kFloydBits), one thread
-      // draws; then ascending positions are compacted
-      for (int i = threadIdx.x; i < (D + 31) / 32; i += blockDim.x) s_pick[i] = 0u;
+      // Floyd's k-subset: for j = D-T .. D-1 draw t in [0, j]; keep t unless
+      // already picked, else keep j.  Membership over a D-bit shared bitmap
+      // (D <= kFloydBits), or by scanning the <= T picks so far (any D); one
+      // thread draws, then the picked positions become neighbour ids.
+      const bool bitmap = D <= kFloydBits;
+      if (bitmap)
+        for (int i = threadIdx.x; i < (D + 31) / 32; i += blockDim.x) s_pick[i] = 0u;
       if (threadIdx.x == 0) s_fill = 0;
       __syncthreads();
       if (threadIdx.x == 0) {
@@ -579,17 +583,32 @@ __global__ void __launch_bounds__(256)
         g1.seed(nk, sd);
         g2.seed(nk, sd);
         g3.seed(nk, sd);
+        int n = 0;
         for (int j = D - T; j < D; ++j) {
           const uint32_t n1 = (uint32_t)(j + 1);
           const int t = (int)(prng == kPcg32 ? g1.bounded(n1)
                                               : prng == kSfc64 ? g2.bounded(n1) : g3.bounded(n1));
-          const int pick = ((s_pick[t >> 5] >> (t & 31)) & 1u) ? j : t;
-          s_pick[pick >> 5] |= 1u << (pick & 31);
+          bool seen;
+          if (bitmap) {
+            seen = (s_pick[t >> 5] >> (t & 31)) & 1u;
+          } else {
+            seen = false;
+            for (int q = 0; q < n; ++q) seen |= s_val[q] == t;
+          }
+          const int pick = seen ? j : t;
+          if (bitmap)
+            s_pick[pick >> 5] |= 1u << (pick & 31);
+          else
+            s_val[n++] = pick;
         }
       }
       __syncthreads();
-      for (int p = threadIdx.x; p < D; p += blockDim.x)
-        if ((s_pick[p >> 5] >> (p & 31)) & 1u) s_val[atomicAdd(&s_fill, 1)] = indices[a + p];
+      if (bitmap) {
+        for (int p = threadIdx.x; p < D; p += blockDim.x)
+          if ((s_pick[p >> 5] >> (p & 31)) & 1u) s_val[atomicAdd(&s_fill, 1)] = indices[a + p];
+      } else {
+        for (int i = threadIdx.x; i < T; i += blockDim.x) s_val[i] = indices[a + s_val[i]];
+      }
     } else {
       // radix-select the T-th smallest key (8 passes of 8 bits), then keep
       // every position whose key is <= it: exactly T positions.

@@ -107,8 +107,6 @@ class BlockSampler:
             raise ValueError("fanouts must be >= 1")
         if prng not in _lib.PRNG_KINDS:
             raise ValueError(f"unknown prng {prng!r} (one of {sorted(_lib.PRNG_KINDS)})")
-        if prng != "splitmix" and max(int(f) for f in fanouts) > 32 and dg.max_degree > 65536:
-            raise NotImplementedError("PRNG variants with fanout > 32 need degree <= 65536")
         self.prng = prng
         self.prng_code = _lib.PRNG_KINDS[prng]
         self.dg = dg
@@ -139,11 +137,20 @@ class BlockSampler:
         self.meta = torch.empty((G * max(caps[:-1]) + 1, 4), dtype=I32, device=dev)
 
     def set_seeds(self, b: int, seeds: np.ndarray, rng_seed: int) -> None:
-        """Host seeds for slot b (API path; the plan path fills on device)."""
-        s = torch.from_numpy(np.ascontiguousarray(seeds, dtype=np.int32))
-        self.seeds[b, : len(s)].copy_(s, non_blocking=False)
-        self.nseeds[b] = len(s)
-        self.rng[b] = int(np.uint64(rng_seed & (2**64 - 1)).astype(np.int64))
+        """Host seeds for slot b (API path; the plan path fills on device):
+        one H2D copy of [seeds | count | rng seed], then device-side scatter."""
+        seeds = np.asarray(seeds)
+        n = len(seeds)
+        if n > self.caps[0]:
+            raise ValueError(f"{n} seeds exceed the sampler capacity {self.caps[0]}")
+        host = np.empty(n + 3, dtype=np.int32)
+        host[:n] = seeds
+        host[n] = n
+        host[n + 1:n + 3] = np.array([rng_seed & (2**64 - 1)], dtype=np.uint64).view(np.int32)
+        dev = torch.from_numpy(host).to(self.dg.device)
+        self.seeds[b, :n].copy_(dev[:n])
+        self.nseeds[b: b + 1].copy_(dev[n:n + 1])
+        self.rng[b: b + 1].copy_(dev[n + 1:n + 3].view(torch.int64))
 
     def run(self, ngroup: int | None = None) -> None:
         """Sample all L levels for slots [0, ngroup) on the current stream."""

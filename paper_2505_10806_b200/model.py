@@ -16,7 +16,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from .aggregate import sage_mean, sage_mean_backward
+from .aggregate import sage_mean, sage_mean_backward, sage_positions
 
 
 @dataclass
@@ -52,12 +52,14 @@ def init_params(feat_dim: int, hidden_dim: int, num_classes: int, num_layers: in
 @dataclass
 class DeviceBlock:
     """One sampled block on the device: frontiers[d] (int32 ids, sorted),
-    ELL edges per level (ell[d]: n_d x F_d, cnt[d]: n_d), fanouts per step."""
+    ELL edges per level (ell[d]: n_d x F_d, cnt[d]: n_d), fanouts per step,
+    and the graph's node count (size of the position-rank scratch)."""
 
     frontiers: list[torch.Tensor]
     ell: list[torch.Tensor]
     cnt: list[torch.Tensor]
     step_fan: list[int]
+    num_nodes: int
 
     @property
     def num_layers(self) -> int:
@@ -69,20 +71,22 @@ def block_from_slot(smp, slot: int, nfront: np.ndarray) -> DeviceBlock:
     fr = [smp.front[d][slot, : int(nfront[d])] for d in range(smp.L + 1)]
     ell = [smp.ell[d][slot] for d in range(smp.L)]
     cnt = [smp.cnt[d][slot, : int(nfront[d])] for d in range(smp.L)]
-    return DeviceBlock(fr, ell, cnt, list(smp.step_fan))
+    return DeviceBlock(fr, ell, cnt, list(smp.step_fan), smp.dg.n)
 
 
 def _forward(block: DeviceBlock, h: torch.Tensor, params: list[LayerParams]):
+    """h: the bundle rows [|input|, >= feat_dim] (a row-strided view is fine)."""
     L = len(params)
     saved = []
+    rank = torch.empty(block.num_nodes, dtype=torch.int32, device=h.device)
     for l, p in enumerate(params):
         d = L - 1 - l
         src_front, dst_front = block.frontiers[d + 1], block.frontiers[d]
-        F = block.step_fan[d]
-        mean, h_self, self_pos = sage_mean(h, src_front, dst_front, block.ell[d], block.cnt[d], F,
-                                           H=p.w_self.shape[0])
+        pos = sage_positions(src_front, dst_front, block.ell[d], block.cnt[d], block.step_fan[d],
+                             block.num_nodes, rank)
+        mean, h_self = sage_mean(h, pos, block.cnt[d], H=p.w_self.shape[0])
         z = h_self @ p.w_self + mean @ p.w_neigh + p.bias
-        saved.append((h, h_self, mean, z, self_pos))
+        saved.append((h, h_self, mean, z, pos))
         h = torch.clamp_min(z, 0) if l < L - 1 else z
     return h, saved
 
@@ -107,7 +111,7 @@ def loss_and_grad(block: DeviceBlock, rows: torch.Tensor, labels: torch.Tensor,
     grads: list[LayerParams | None] = [None] * L
     for l in range(L - 1, -1, -1):
         p = params[l]
-        h, h_self, mean, z, self_pos = saved[l]
+        h, h_self, mean, z, pos = saved[l]
         if l < L - 1:
             dz = dz * (z > 0)
         grads[l] = LayerParams(h_self.T @ dz, mean.T @ dz, dz.sum(dim=0))
@@ -115,8 +119,7 @@ def loss_and_grad(block: DeviceBlock, rows: torch.Tensor, labels: torch.Tensor,
             d = L - 1 - l
             dself = dz @ p.w_self.T
             dmean = dz @ p.w_neigh.T
-            dz = sage_mean_backward(dself, dmean, block.cnt[d], self_pos, block.frontiers[d + 1],
-                                    block.ell[d], block.step_fan[d])
+            dz = sage_mean_backward(dself, dmean, block.cnt[d], pos)
     return loss, grads
 
 

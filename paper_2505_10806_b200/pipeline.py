@@ -14,6 +14,9 @@ cache fill -> cache route) follows train.py:190-204 / cache.py:80-148.
 
 from __future__ import annotations
 
+import queue
+import threading
+import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -203,7 +206,14 @@ class WorkerPipeline:
         return threshold_select(counts, bm, hist.cpu().numpy().astype(np.int64), n_hot)
 
     def build_cache(self, hot_ids: torch.Tensor) -> HotCache:
-        """VectorPull of the hot rows + cache route (cache.py:139-148)."""
+        """VectorPull of the hot rows + cache route (cache.py:139-148),
+        installed as the steady cache."""
+        self.cache = self.make_cache(hot_ids)
+        return self.cache
+
+    def make_cache(self, hot_ids: torch.Tensor) -> HotCache:
+        """A cache buffer for hot_ids on the current stream, not installed
+        (the secondary of the double buffer, cache.py:80-104)."""
         st = self.store
         n_hot = int(hot_ids.numel())
         rows = torch.empty((max(n_hot, 1), st.src_stride), dtype=torch.float32,
@@ -230,8 +240,7 @@ class WorkerPipeline:
                           st.peer_mask, ptr(rows), ptr(cnt), s)
             c = cnt.cpu().numpy()[0].view(np.uint32)
             rpcs = bin(int(c[_lib.RG_CNT_OWNER_MASK])).count("1")
-        self.cache = HotCache(hot_ids, rows, route, (rpcs, n_hot, 4 * st.d * n_hot))
-        return self.cache
+        return HotCache(hot_ids, rows, route, (rpcs, n_hot, 4 * st.d * n_hot))
 
     def start_epoch(self, schedule: SeedSchedule, e: int) -> None:
         self.epoch = e
@@ -273,68 +282,6 @@ class WorkerPipeline:
         gr.replay()
         return ng
 
-    def enable_staging(self, rank: int, world: int) -> None:
-        """Staged multi-GPU mode (rg_stage_rows / rg_gather_bundle_staged):
-        two chunk-aligned staging buffers, mapped on every rank."""
-        from . import multigpu
-
-        st = self.store
-        self.rank, self.world = rank, world
-        self.staging = [torch.empty((self.G, self.cap_in, st.stride), dtype=torch.float32,
-                                    device=self.dg.device) for _ in range(2)]
-        self.stage_ptrs = multigpu.exchange_buffers(self.staging, rank, world)
-        self.mine_mask = sum(1 << q for q in range(st.k) if q % world == rank)
-        rank_of = np.zeros(16, dtype=np.uint8)
-        rank_of[: st.k] = [q % world for q in range(st.k)]
-        self.rank_of = rank_of
-
-    def stage(self, ng: int, smp, slot: int) -> None:
-        """Owner side: this GPU's rows of the group into staging[slot]."""
-        st = self.store
-        _lib.call("rg_stage_rows", ptr(smp.front[smp.L]), ptr(smp.nfront[smp.L]), self.cap_in, ng,
-                  ptr(st.route), bases_array(st.bases), self.mine_mask,
-                  st.src_stride, st.stride, ptr(self.staging[slot]), _lib.stream_handle())
-
-    def gather_staged(self, ng: int, i0: int, smp, slot: int, rows) -> None:
-        """Consumer side: peer rows from the owners' staging[slot]."""
-        st = self.store
-        route = st.route
-        b = list(st.bases)
-        if self.cache is not None and self.cache.hot_ids.numel():
-            b[_lib.RG_KIND_CACHE] = self.cache.rows.data_ptr()
-            route = self.cache.route
-        stage = np.zeros(8, dtype=np.uint64)
-        stage[: self.world] = self.stage_ptrs[slot]
-        _lib.call("rg_gather_bundle_staged", ptr(smp.front[smp.L]), ptr(smp.nfront[smp.L]),
-                  self.cap_in, ng, ptr(route), ptr(st.owner), bases_array(b),
-                  stage.ctypes.data, self.rank_of.ctypes.data, self.rank, st.src_stride, st.stride,
-                  self.my_part, st.peer_mask, ptr(rows),
-                  ptr(self.counters) + i0 * _lib.RG_NCOUNTERS * 4, _lib.stream_handle())
-
-    def step_staged(self, i0: int, barrier, events=None, fill: bool = True) -> int:
-        """Sample, stage this GPU's rows of the group, barrier (every owner
-        staged), then gather with peer rows read from the owners' staging
-        buffers.  Buffers alternate per step; the synchronize before the
-        barrier also guarantees the previous step's readers are done.
-        fill=False: the caller already placed the group's seeds."""
-        ng = min(self.G, self.nb - i0)
-        slot = self.k % 2
-        self.k += 1
-        smp = self.samplers[slot % self.nbuf]
-        if fill:
-            self.plan.fill(self.perm, self.epoch, i0, ng, smp)
-        smp.run(ng)
-        self.stage(ng, smp, slot)
-        torch.cuda.current_stream().synchronize()
-        barrier()
-        if events is not None:
-            events[0].record()
-        self.gather_staged(ng, i0, smp, slot, self.row_bufs[slot % self.nbuf])
-        if events is not None:
-            events[1].record()
-        self.launches += 1 + 1 + 2 + smp.L * 3 + 2
-        return ng
-
     def step_overlapped(self, i0: int, host_seeds=None) -> int:
         """Like step(), but sampling and gather of consecutive groups overlap
         on two streams (buffer k % nbuf).  Call sync_streams() before reading
@@ -345,6 +292,7 @@ class WorkerPipeline:
         ng = min(self.G, self.nb - i0)
         slot = self.k % self.nbuf
         self.k += 1
+        self.last_slot = slot
         smp = self.samplers[slot]
         tl = self.timeline
 
@@ -380,6 +328,15 @@ class WorkerPipeline:
             self.ev_gathered[slot].record(self.s_gather)
         self.launches += 1 + 1 + 2 + smp.L * 3 + 1
         return ng
+
+    def acquire(self, slot: int) -> None:
+        """Current stream waits until group `slot` is sampled and gathered."""
+        torch.cuda.current_stream().wait_event(self.ev_gathered[slot])
+
+    def release(self, slot: int) -> None:
+        """The current stream's queued work is the last reader of `slot`:
+        the next step_overlapped into it waits for that work."""
+        self.ev_gathered[slot].record(torch.cuda.current_stream())
 
     def enter_streams(self) -> None:
         """Order both side streams after the current stream's work."""
@@ -427,6 +384,91 @@ class WorkerPipeline:
         return {"local": int(c[:, 0].sum()), "hit": int(c[:, 1].sum()),
                 "fallback": int(c[:, 2].sum()), "bad": int(c[:, 4].sum()), "rpcs": rpcs,
                 "peer": int(c[:, _lib.RG_CNT_PEER].sum()), "per_batch": c}
+
+
+class GroupProducer:
+    """Producer thread of the device pipeline (prefetch.py:91-164 at group
+    granularity): samples and gathers groups i0 = starts[0], starts[1], ...
+    on the pipeline's side streams (step_overlapped) while the consumer
+    trains the previous group on its own stream.  At most nbuf groups are
+    live: a slot is produced into again only after the consumer released it
+    (token per slot), and its device reuse is ordered by the consumer's
+    release event.  The host wait for a group's sizes (nfront) happens on
+    this thread, never on the consumer's.  latency_ms > 0 sleeps the
+    injected per-request latency (store.py:73-74) here, once per fallback
+    RPC of the group, so the producer hides it like the reference's
+    Prefetcher thread does."""
+
+    def __init__(self, pipe: WorkerPipeline, starts, latency_ms: float = 0.0):
+        if pipe.nbuf < 2:
+            raise ValueError("GroupProducer needs a double-buffered pipeline (nbuf >= 2)")
+        self.pipe = pipe
+        self.latency_ms = float(latency_ms)
+        self._q: queue.Queue = queue.Queue()
+        self._tokens = threading.Semaphore(pipe.nbuf)
+        self._stop = threading.Event()
+        self._done = False
+        pin = torch.cuda.is_available()
+        self._nf = [torch.zeros((pipe.sampler.L + 1, pipe.G), dtype=I32).pin_memory()
+                    if pin else None for _ in range(pipe.nbuf)]
+        self._cnt = [torch.zeros((pipe.G, _lib.RG_NCOUNTERS), dtype=I32).pin_memory()
+                     if pin else None for _ in range(pipe.nbuf)]
+        self._ev = [torch.cuda.Event() for _ in range(pipe.nbuf)]
+        self._dev = torch.cuda.current_device()
+        pipe.enter_streams()
+        self._t = threading.Thread(target=self._run, args=(list(starts),), daemon=True)
+        self._t.start()
+
+    def _run(self, starts) -> None:
+        pipe = self.pipe
+        try:
+            torch.cuda.set_device(self._dev)
+            for i0 in starts:
+                while not self._tokens.acquire(timeout=0.05):
+                    if self._stop.is_set():
+                        return
+                if self._stop.is_set():
+                    return
+                ng = pipe.step_overlapped(i0)
+                slot = pipe.last_slot
+                with torch.cuda.stream(pipe.s_gather):
+                    self._nf[slot].copy_(pipe.samplers[slot].nfront, non_blocking=True)
+                    if self.latency_ms > 0:
+                        self._cnt[slot][:ng].copy_(pipe.counters[i0:i0 + ng], non_blocking=True)
+                    self._ev[slot].record(pipe.s_gather)
+                self._ev[slot].synchronize()
+                if self.latency_ms > 0:
+                    masks = self._cnt[slot][:ng, _lib.RG_CNT_OWNER_MASK].numpy().view(np.uint32)
+                    rpcs = sum(bin(int(m)).count("1") for m in masks)
+                    time.sleep(self.latency_ms * rpcs / 1000.0)
+                self._q.put((i0, ng, slot, self._nf[slot][:, :ng].numpy().copy()))
+            self._q.put(None)
+        except BaseException as exc:  # surfaced on the consumer side
+            self._q.put(exc)
+
+    def next_group(self):
+        """(i0, ng, slot, nfront [L+1, ng]) of the next group, its rows usable
+        on the current stream; None at the end."""
+        if self._done:
+            return None
+        item = self._q.get()
+        if item is None:
+            self._done = True
+            return None
+        if isinstance(item, BaseException):
+            self._done = True
+            raise item
+        self.pipe.acquire(item[2])
+        return item
+
+    def release(self, slot: int) -> None:
+        self.pipe.release(slot)
+        self._tokens.release()
+
+    def close(self) -> None:
+        self._stop.set()
+        self._t.join()
+        self.pipe.sync_streams()
 
 
 def run_accounting(g, book, fanouts, batch_size: int, epochs: int, s0: int, mode: str = "rapid",

@@ -111,20 +111,28 @@ def _sampler_for(dg: DeviceGraph, fanouts, n_seeds: int, prng: str = "splitmix")
 
 def block_from_sampler(smp: BlockSampler, slot: int, seeds: np.ndarray, epoch: int,
                        batch: int) -> ComputationBlock:
-    """Materialise slot `slot` of a sampler run as a numpy ComputationBlock."""
-    nf = smp.nfront[:, slot].cpu().numpy()
-    for d in range(smp.L + 1):
+    """Materialise slot `slot` of a sampler run as a numpy ComputationBlock:
+    flat edges per level on the device, one D2H of the sizes, one packed D2H
+    of every frontier and edge array."""
+    L = smp.L
+    lv = [smp.edges(d, slot + 1) for d in range(L)]
+    sizes = torch.cat([smp.nfront[:, slot]] + [e[2][slot:slot + 1] for e in lv]).cpu().numpy()
+    nf, ne = sizes[:L + 1], sizes[L + 1:]
+    for d in range(L + 1):
         if nf[d] > smp.caps[d]:
             raise RuntimeError(f"frontier {d} overflow ({nf[d]} > {smp.caps[d]})")
-    frontiers = [smp.front[d][slot, : nf[d]].cpu().numpy().astype(np.int64)
-                 for d in range(smp.L + 1)]
-    edges = []
-    for d in range(smp.L):
-        src, dst, nedge = smp.edges(d)
-        ne = int(nedge[slot])
-        edges.append((src[slot, :ne].cpu().numpy().astype(np.int64),
-                      dst[slot, :ne].cpu().numpy().astype(np.int64)))
-    input_dev = smp.front[smp.L][slot, : nf[smp.L]].clone()
+    parts = [smp.front[d][slot, : nf[d]] for d in range(L + 1)]
+    for d in range(L):
+        parts += [lv[d][0][slot, : ne[d]], lv[d][1][slot, : ne[d]]]
+    flat = torch.cat(parts)
+    host = torch.empty(flat.shape, dtype=flat.dtype, pin_memory=True)
+    host.copy_(flat)
+    out = host.numpy().astype(np.int64)
+    cuts = np.cumsum([int(p.numel()) for p in parts])[:-1]
+    pieces = np.split(out, cuts)
+    frontiers = pieces[:L + 1]
+    edges = [(pieces[L + 1 + 2 * d], pieces[L + 2 + 2 * d]) for d in range(L)]
+    input_dev = parts[L].clone()
     return ComputationBlock(epoch=epoch, batch=batch, seeds=seeds, frontiers=frontiers,
                             edges=edges, device={"input_nodes": input_dev})
 

@@ -85,13 +85,17 @@ class StoreShard:
         out = gather_rows(self.rows_device, pos.astype(np.int32), self.src_stride, self.stride)
         return out[:, : self.feat_dim].cpu().numpy()
 
-    def _served(self, nodes: int) -> None:
+    def _served(self, nodes: int | None) -> None:
+        """One handled request (store.py:71-88): the injected latency is
+        slept per request; nodes=None when the bundle gather served it
+        (rows read in place, per-owner row counts not materialised)."""
         if self.latency_ms > 0:
             time.sleep(self.latency_ms / 1000.0)
         with self._lock:
             self.rpc_calls += 1
-            self.nodes_served += nodes
-            self.payload_bytes += bytes_for(nodes, self.feat_dim)
+            if nodes is not None:
+                self.nodes_served += nodes
+                self.payload_bytes += bytes_for(nodes, self.feat_dim)
 
 
 class InprocTransport:
@@ -193,6 +197,17 @@ class StoreClient:
         if account is not None:
             account.charge(rpcs, n, self.feat_dim)
         return out, rpcs
+
+    def served(self, owner_mask: int) -> None:
+        """Requests the bundle gather made: one per owner bit set."""
+        q = 0
+        while owner_mask:
+            if owner_mask & 1 and q < len(self._shards):
+                s = self._shards[q]
+                if isinstance(s, StoreShard):
+                    s._served(None)
+            owner_mask >>= 1
+            q += 1
 
     def sync_pull(self, node_ids: np.ndarray, account: TransferAccount | None = None) -> np.ndarray:
         """On-demand pull; rows come back in request order (store.py:198-201)."""

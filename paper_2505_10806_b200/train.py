@@ -15,6 +15,7 @@ after the other on this GPU (or one per GPU under bench.py / torchrun).
 from __future__ import annotations
 
 import csv
+import threading
 import time
 from dataclasses import dataclass, field
 
@@ -26,7 +27,7 @@ from .engine import DeviceGraph, FeatureStore
 from .graph import load_graph, synth_powerlaw
 from .partition import (halo_expand, load_partition, partition_edgecut,
                         partition_random)
-from .pipeline import WorkerPipeline, resolve_n_hot
+from .pipeline import GroupProducer, WorkerPipeline, resolve_n_hot
 from .plan import candidates, generate_plan
 from .rng import mix64
 from .sampler import SeedSchedule
@@ -106,6 +107,7 @@ class RunConfig:
     # B200 additions
     prng: str = "splitmix"
     group: int = 16
+    overlap: bool = True  # sample+gather group k+1 while group k trains (GroupProducer)
 
     def validate(self) -> None:
         """train.py:121-135."""
@@ -180,7 +182,7 @@ def _run(cfg: RunConfig) -> list[WorkerResult]:
     counts = None
     for p in range(k):
         pipe = WorkerPipeline(dg, store, p, train, cfg.fanouts, cfg.batch_size, cfg.s0,
-                              cfg.group, nbuf=1, prng=cfg.prng)
+                              cfg.group, nbuf=2 if cfg.overlap else 1, prng=cfg.prng)
         nb = pipe.nb
         sched = SeedSchedule(cfg.s0, cfg.epochs, nb)
         if counts is None:  # the plan pass (and its digest) is shared by all workers
@@ -202,31 +204,67 @@ def _run(cfg: RunConfig) -> list[WorkerResult]:
         hits_acc = misses_acc = 0
         records = []
         cache_keys = None
+        secondary = None  # (thread, result dict) building epoch e+1's cache
         for e in range(cfg.epochs):
             t0 = time.perf_counter()
             if rapid and (cfg.hot_scope == "epoch" or e == 0):
-                scope = counts[e] if cfg.hot_scope == "epoch" else counts_all
-                hot = pipe.select_hot(scope, n_hot, max_count)
-                cache = pipe.build_cache(hot)
+                if secondary is not None:  # cache.py:106-129: join, swap
+                    secondary[0].join()
+                    if "error" in secondary[1]:
+                        raise secondary[1]["error"]
+                    hot, cache = secondary[1]["hot"], secondary[1]["cache"]
+                    pipe.cache = cache
+                    secondary = None
+                else:
+                    scope = counts[e] if cfg.hot_scope == "epoch" else counts_all
+                    hot = pipe.select_hot(scope, n_hot, max_count)
+                    cache = pipe.build_cache(hot)
                 if cache.fill[1]:
                     fill = [fill[0] + cache.fill[0], fill[1] + cache.fill[1],
                             fill[2] + 4 * g.feat_dim * cache.fill[1]]
                 if e == 0 and cfg.dump_cache_keys:
                     cache_keys = hot.cpu().numpy().astype(np.int64)
+            if rapid and cfg.hot_scope == "epoch" and e + 1 < cfg.epochs:
+                secondary = _start_secondary(pipe, counts[e + 1], n_hot, max_count)
             pipe.start_epoch(sched, e)
             loss_sum = torch.zeros((), dtype=torch.float64, device=dg.device)
-            smp = pipe.sampler
-            for i0 in range(0, nb, pipe.G):
-                ng = pipe.step(i0)
-                nf = smp.nfront[:, :ng].cpu().numpy()
+
+            def train_group(smp, rows_buf, ng, nf):
+                nonlocal params
                 for b in range(ng):
                     blk = model.block_from_slot(smp, b, nf[:, b])
-                    rows = pipe.rows[b, : int(nf[smp.L, b]), : g.feat_dim]
+                    rows = rows_buf[b, : int(nf[smp.L, b]), : g.feat_dim]
                     if dtype != torch.float32:
                         rows = rows.to(dtype)
                     loss, grads = model.loss_and_grad(blk, rows, labels, params)
                     params = model.sgd_step(params, grads, cfg.lr)
-                    loss_sum += loss.double()
+                    loss_sum.add_(loss.double())
+
+            starts = range(0, nb, pipe.G)
+            if cfg.overlap:
+                # rapid: the producer thread sleeps the injected latency (hidden
+                # behind training, prefetch.py:116-132); baseline pulls inline
+                # in the worker (train.py:223-230), so its latency is not hidden
+                prod = GroupProducer(pipe, starts, cfg.latency_ms if rapid else 0.0)
+                try:
+                    while (item := prod.next_group()) is not None:
+                        i0, ng, slot, nf = item
+                        if not rapid and cfg.latency_ms > 0:
+                            _sleep_rpcs(pipe, i0, ng, cfg.latency_ms)
+                        train_group(pipe.samplers[slot], pipe.row_bufs[slot], ng, nf)
+                        prod.release(slot)
+                finally:
+                    prod.close()
+            else:
+                smp = pipe.sampler
+                for i0 in starts:
+                    ng = pipe.step(i0)
+                    nf = smp.nfront[:, :ng].cpu().numpy()
+                    if cfg.latency_ms > 0:
+                        _sleep_rpcs(pipe, i0, ng, cfg.latency_ms)
+                    train_group(smp, pipe.rows, ng, nf)
+            if secondary is not None:
+                secondary[0].join()  # the epoch includes the wait (train.py:233)
             t = pipe.totals()
             nodes = t["fallback"]
             if rapid:
@@ -254,6 +292,41 @@ def _run(cfg: RunConfig) -> list[WorkerResult]:
         for r in results:
             write_metrics(r.records, worker_metrics_path(cfg.metrics_out, r.part))
     return results
+
+
+def _start_secondary(pipe: WorkerPipeline, counts: torch.Tensor, n_hot: int, max_count: int):
+    """Build the next epoch's cache (top_hot of its access counts, then the
+    VectorPull) on a background thread and its own stream while the current
+    epoch runs (cache.py:80-104); joined and swapped at the epoch boundary."""
+    out: dict = {}
+    dev = torch.cuda.current_device()
+    ready = torch.cuda.Event()
+    ready.record()  # counts / store are complete on the caller's stream
+
+    def build():
+        try:
+            torch.cuda.set_device(dev)
+            stream = torch.cuda.Stream()
+            with torch.cuda.stream(stream):
+                stream.wait_event(ready)
+                hot = pipe.select_hot(counts, n_hot, max_count)
+                out["cache"] = pipe.make_cache(hot)
+                out["hot"] = hot
+            stream.synchronize()
+        except BaseException as exc:  # re-raised by the epoch loop
+            out["error"] = exc
+
+    t = threading.Thread(target=build, daemon=True)
+    t.start()
+    return t, out
+
+
+def _sleep_rpcs(pipe: WorkerPipeline, i0: int, ng: int, latency_ms: float) -> None:
+    """Injected per-request latency (store.py:73-74) for the group's fallback
+    pulls, slept on the calling thread."""
+    masks = pipe.counters[i0:i0 + ng, 3].cpu().numpy().view(np.uint32)
+    rpcs = sum(bin(int(m)).count("1") for m in masks)
+    time.sleep(latency_ms * rpcs / 1000.0)
 
 
 def worker_metrics_path(path: str, part: int) -> str:

@@ -396,33 +396,81 @@ def test_star_marginal_uniformity(rg):
         assert np.array_equal(np.sort(picks[s]), ed[0][0])
 
 
-def test_sage_mean_fwd_bwd_bit_exact(rg):
-    """K8 against the reference's in-order numpy semantics (model.py:72-81, 126-135)."""
+def _sage_check(rg, blk, h0, dtype, rng, hidden=48):
     from paper_2505_10806_b200.aggregate import edges_to_ell, sage_mean, sage_mean_backward
+    from paper_2505_10806_b200.aggregate import sage_positions
 
-    g = rg.synth_powerlaw(20000, 5, 64, 8, seed=7)
-    rng = np.random.default_rng(11)
-    blk = rg.sample_block(g, rng.choice(20000, 256, replace=False), [10, 25], 99)
-    h0 = g.features[blk.input_nodes]
+    n_nodes = int(max(int(f.max()) for f in blk.frontiers if len(f))) + 1
     for d in range(blk.num_layers - 1, -1, -1):
         src_front, dst_front = blk.frontiers[d + 1], blk.frontiers[d]
         src, dst = blk.edges[d]
         h = h0 if d == blk.num_layers - 1 else rng.standard_normal(
-            (len(src_front), 48)).astype(np.float32)
+            (len(src_front), hidden)).astype(dtype)
         want_mean, want_self = orc.mean_aggregate(h, src_front, dst_front, src, dst)
         ell, cnt, F = edges_to_ell(dst_front, src, dst)
         dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
-        mean, hself, self_pos = sage_mean(dev(h), dev(src_front.astype(np.int32)),
-                                          dev(dst_front.astype(np.int32)), dev(ell), dev(cnt), F)
+        pos = sage_positions(dev(src_front.astype(np.int32)), dev(dst_front.astype(np.int32)),
+                             dev(ell), dev(cnt), F, n_nodes)
+        mean, hself = sage_mean(dev(h), pos, dev(cnt))
         assert np.array_equal(mean.cpu().numpy(), want_mean)
         assert np.array_equal(hself.cpu().numpy(), want_self)
-        dself = rng.standard_normal(want_mean.shape).astype(np.float32)
-        dmean = rng.standard_normal(want_mean.shape).astype(np.float32)
+        dself = rng.standard_normal(want_mean.shape).astype(dtype)
+        dmean = rng.standard_normal(want_mean.shape).astype(dtype)
         want_dh = orc.mean_aggregate_bwd(dself, dmean, len(src_front), src_front, dst_front,
                                          src, dst)
-        dh = sage_mean_backward(dev(dself), dev(dmean), dev(cnt), self_pos,
-                                dev(src_front.astype(np.int32)), dev(ell), F)
+        dh = sage_mean_backward(dev(dself), dev(dmean), dev(cnt), pos)
         assert np.array_equal(dh.cpu().numpy(), want_dh)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_sage_mean_fwd_bwd_bit_exact(rg, dtype):
+    """K8 against the reference's in-order numpy semantics (model.py:72-81,
+    126-135), fp32 and fp64 (RunConfig.precision)."""
+    g = rg.synth_powerlaw(20000, 5, 64, 8, seed=7)
+    rng = np.random.default_rng(11)
+    blk = rg.sample_block(g, rng.choice(20000, 256, replace=False), [10, 25], 99)
+    _sage_check(rg, blk, g.features[blk.input_nodes].astype(dtype), dtype, rng)
+
+
+def test_sage_mean_hub_in_degree_above_4096(rg):
+    """A star centre sampled by > 4,096 dst rows: its backward segment is
+    longer than any shared-memory sort (the round-1 kernel flagged it and
+    went on silently); the radix-sort transpose keeps it bit-exact."""
+    n_leaf = 6000
+    edges = [(0, j) for j in range(1, n_leaf + 1)]
+    g = rg.from_edge_list(n_leaf + 1, edges, feat_dim=20)
+    rng = np.random.default_rng(5)
+    g.features[:] = rng.standard_normal(g.features.shape).astype(np.float32)
+    blk = rg.sample_block(g, np.arange(1, n_leaf + 1), [3], 17)
+    src, dst = blk.edges[0]
+    assert int((src == 0).sum()) == n_leaf  # every leaf's only neighbour is the hub
+    _sage_check(rg, blk, g.features[blk.input_nodes], np.float32, rng)
+
+
+def test_sage_mean_strided_rows(rg):
+    """the forward reads h with its row pitch (h.stride(0)), so a
+    view of padded bundle rows with feat_dim % 4 != 0 (d = 6, the reference's
+    acceptance graph) aggregates the right rows."""
+    from paper_2505_10806_b200.aggregate import edges_to_ell, sage_mean, sage_positions
+
+    g = rg.synth_powerlaw(3000, 4, 6, 3, seed=7)
+    rng = np.random.default_rng(2)
+    blk = rg.sample_block(g, rng.choice(3000, 64, replace=False), [5, 4], 3)
+    src_front, dst_front = blk.frontiers[2], blk.frontiers[1]
+    src, dst = blk.edges[1]
+    h = g.features[src_front]
+    padded = np.zeros((len(src_front), 8), np.float32)
+    padded[:, :6] = h
+    view = torch.from_numpy(padded).cuda()[:, :6]
+    assert view.stride(0) == 8
+    want_mean, want_self = orc.mean_aggregate(h, src_front, dst_front, src, dst)
+    ell, cnt, F = edges_to_ell(dst_front, src, dst)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    pos = sage_positions(dev(src_front.astype(np.int32)), dev(dst_front.astype(np.int32)),
+                         dev(ell), dev(cnt), F, g.num_nodes)
+    mean, hself = sage_mean(view, pos, dev(cnt))
+    assert np.array_equal(mean.cpu().numpy(), want_mean)
+    assert np.array_equal(hself.cpu().numpy(), want_self)
 
 
 @pytest.mark.parametrize("kind", ["pcg32", "sfc64", "xoshiro256pp"])
@@ -530,6 +578,99 @@ def test_products_full_size(products):
     assert t["rpcs"] == 11_725
 
 
+def test_products_reference_goldens(rg, products):
+    """Products scale, pinned to the REFERENCE's own outputs at the metric's
+    configuration (tests/golden/make_golden_products.py ran gnnpipe's
+    sample_block / collect_access / top_hot / assemble_bundle over the whole
+    epoch): every batch's input_nodes and the plan digest, the access table
+    of all 8 workers, the hot sets at 5/10/15/20/65 % and worker 0's per-batch
+    accounting (local, hit, fallback, RPCs) at 0/5/10/15/20/65 %, all
+    bit-exact (plan.py:72-141, prefetch.py:41-88, train.py:165-168)."""
+    import json
+    from pathlib import Path
+
+    from paper_2505_10806_b200 import _lib
+    from paper_2505_10806_b200.pipeline import WorkerPipeline, resolve_n_hot
+    from paper_2505_10806_b200.plan import candidates, threshold_select
+    from paper_2505_10806_b200.sampler import SeedSchedule
+
+    gold_dir = Path(__file__).resolve().parent / "golden"
+    gold = json.loads((gold_dir / "products.json").read_text())
+    z = np.load(gold_dir / "products_w0.npz")
+    h16 = lambda *a: hashlib.blake2b(b"".join(np.ascontiguousarray(x).tobytes()  # noqa: E731
+                                              for x in a), digest_size=16).hexdigest()
+    g, dg, store = products
+    owner = np.asarray(store.owner_np)
+    train = np.flatnonzero(g.train_mask)
+    pipe = WorkerPipeline(dg, store, 0, train, [15, 10, 5], 1024, 7, 32, nbuf=1)
+    nb = pipe.nb
+    assert nb == gold["config"]["batches"]
+    sched = SeedSchedule(7, 1, nb)
+
+    # every batch's input nodes + the reference plan digest
+    pipe.start_epoch(sched, 0)
+    smp = pipe.sampler
+    dig = hashlib.blake2b(digest_size=8)
+    total = 0
+    for i0 in range(0, nb, pipe.G):
+        ng = pipe.step(i0)
+        nf = smp.nfront[smp.L, :ng].cpu().numpy()
+        front = smp.front[smp.L][:ng].cpu().numpy()
+        for b in range(ng):
+            ids = front[b, : nf[b]].astype("<i8")
+            i = i0 + b
+            assert nf[b] == z["input_len"][i], i
+            assert hashlib.blake2b(ids.tobytes(), digest_size=16).digest() == \
+                z["input_hash"][i].tobytes(), i
+            dig.update(np.array([0, i], dtype="<u8").tobytes())
+            dig.update(ids.astype("<u8").tobytes())
+            total += int(nf[b])
+    assert f"{int.from_bytes(dig.digest(), 'little'):016x}" == gold["plan_digest"]
+    assert total == gold["inputs_total"]
+
+    # collect_access: dense counts (worker independent) and every worker's table
+    counts = pipe.count_epoch(sched, 0)
+    c_np = counts.cpu().numpy()
+    allt = gold["all_nodes_table"]
+    assert h16(c_np.astype("<i4")) == allt["dense_i32"]
+    assert int(c_np.sum()) == allt["accesses"] and int(c_np.max()) == allt["max"]
+    hot_w0 = {}
+    for p in range(8):
+        rec = gold["workers"][str(p)]
+        ids = np.flatnonzero((c_np > 0) & (owner != p))
+        assert len(ids) == rec["n_remote"], p
+        assert h16(ids.astype("<i8"), c_np[ids].astype("<i8")) == rec["table"], p
+        _, nout, hist, bm = candidates(counts, store.owner, p, nb)
+        assert int(nout.item()) == rec["n_remote"]
+        for pct, want in rec["hot"].items():
+            n_hot = resolve_n_hot(float(pct), rec["n_remote"])
+            assert n_hot == want["n_hot"], (p, pct)
+            if p != 0 and pct != "15":
+                continue
+            hot = threshold_select(counts, bm, hist.cpu().numpy().astype(np.int64), n_hot)
+            hot_np = hot.cpu().numpy().astype(np.int64)
+            assert h16(hot_np.astype("<i8")) == want["ids"], (p, pct)
+            if p == 0:
+                hot_w0[int(pct)] = hot
+    want15 = np.cumsum(z["hot15_delta"].astype(np.int64))
+    assert np.array_equal(hot_w0[15].cpu().numpy(), want15)
+
+    # worker 0's per-batch accounting with each steady cache (and none)
+    for pct in [0, 5, 10, 15, 20, 65]:
+        pipe.cache = None if pct == 0 else pipe.build_cache(hot_w0[pct])
+        pipe.start_epoch(sched, 0)
+        for i0 in range(0, nb, pipe.G):
+            pipe.step(i0)
+        c = pipe.totals()["per_batch"]
+        rpcs = np.array([bin(int(m)).count("1") for m in c[:, _lib.RG_CNT_OWNER_MASK]])
+        got = np.stack([c[:, 0], c[:, 1], c[:, 2], rpcs], axis=1)
+        assert np.array_equal(got, z[f"acct_{pct}"]), pct
+        acc = gold["w0_accounting"][str(pct)]
+        assert int(c[:, 2].sum()) == acc["nodes_pulled"] and int(rpcs.sum()) == acc["rpc_calls"]
+        assert int(c[:, 1].sum()) == acc["cache_hits"]
+    pipe.cache = None
+
+
 def test_products_epoch_properties(products):
     """Every batch of a full Products epoch (not just sampled ones), checked
     on the device through size-independent properties of sample_block
@@ -630,7 +771,7 @@ def test_training_mode_equivalence(rg, golden):
             assert torch.equal(pa.bias, pb.bias)
 
 
-@pytest.mark.parametrize("mode", ["prefetch", "nccl", "pull", "staged"])
+@pytest.mark.parametrize("mode", ["prefetch", "nccl", "pull"])
 def test_two_gpu_peer_gather_bit_exact(mode):
     """One process per GPU, peer shards over NVLink (CUDA IPC), with the
     group prefetch into local shadows (NVLink loads, or NCCL all-to-all as
@@ -655,13 +796,11 @@ def test_two_gpu_peer_gather_bit_exact(mode):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(port), str(root / "bench.py"),
            "--gpus", "2", "--steps", "2", "--warmup", "1", "--no-cpu", "--no-e2e", "--check",
-           "--group", "32"]  # correctness run: small groups (staged doubles the bundle memory)
+           "--group", "32"]  # correctness run: small groups
     if mode == "pull":
         cmd.append("--pull")
     elif mode == "nccl":
         cmd += ["--transport", "nccl"]
-    elif mode == "staged":
-        cmd.append("--staged")
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=root,
                          env=dict(os.environ))
     assert out.returncode == 0, out.stderr[-2000:]
@@ -669,7 +808,7 @@ def test_two_gpu_peer_gather_bit_exact(mode):
     assert line["check"]["all_ranks_bit_exact"] is True
     assert line["remote_rows_epoch"]["uncached"] == 933_549_256
     assert line["remote_rows_epoch"]["rpcs"] == 11_725
-    if mode in ("pull", "staged"):
+    if mode == "pull":
         assert line["nvlink"]["peer_rows_per_batch"] > 0
     else:
         assert line["nvlink"]["prefetched_rows_per_batch"] > 0
@@ -789,49 +928,3 @@ def test_group_prefetch_pipeline_single_gpu(rg, products):
         ref.step(i0)
     r = ref.totals()
     assert t["bad"] == 0 and np.array_equal(t["per_batch"][:128, :5], r["per_batch"][:128, :5])
-
-
-def test_tma_gather_matches_gather(rg):
-    """Experimental TMA bulk-copy gather (rg_gather_bundle_tma)
-    produces the same bundle rows and provenance counters as the main
-    gather, incl. cache hits, fallbacks and invalid route words."""
-    from paper_2505_10806_b200 import _lib
-    from paper_2505_10806_b200.engine import bases_array
-
-    gen = torch.Generator().manual_seed(11)
-    n, d, G, cap = 20000, 100, 3, 4000
-    kinds = torch.randint(0, 3, (n,), generator=gen)
-    kinds[torch.randperm(n, generator=gen)[:3000]] = _lib.RG_KIND_CACHE
-    rows_of = torch.zeros(n, dtype=torch.int64)
-    shards = {}
-    for q in (0, 1, 2, _lib.RG_KIND_CACHE):
-        m = kinds == q
-        rows_of[m] = torch.arange(int(m.sum()))
-        shards[q] = torch.randn((int(m.sum()), d), generator=gen).cuda()
-    route = (kinds << 28) | rows_of
-    route[::501] = 0xFFFFFFFF
-    route32 = torch.from_numpy(route.numpy().astype(np.uint32).view(np.int32)).cuda()
-    ids = torch.randint(0, n, (G, cap), generator=gen, dtype=torch.int64).to(torch.int32).cuda()
-    nids = torch.tensor([cap, cap - 17, 1], dtype=torch.int32, device="cuda")
-    b = [0] * 16
-    for q, t in shards.items():
-        b[q] = t.data_ptr()
-    bases = bases_array(b)
-    s = _lib.stream_handle()
-    outs, cnts = [], []
-    for fn in ("rg_gather_bundle", "rg_gather_bundle_tma"):
-        out = torch.full((G, cap, d), -1.0, device="cuda")
-        cnt = torch.zeros((G, _lib.RG_NCOUNTERS), dtype=torch.int32, device="cuda")
-        if fn == "rg_gather_bundle":
-            _lib.call(fn, ids.data_ptr(), nids.data_ptr(), cap, G, route32.data_ptr(), bases, d, d,
-                      0, 0, out.data_ptr(), cnt.data_ptr(), s)
-        else:
-            _lib.call(fn, ids.data_ptr(), nids.data_ptr(), cap, G, route32.data_ptr(), bases, d, d,
-                      0, out.data_ptr(), cnt.data_ptr(), 0, s)
-        outs.append(out)
-        cnts.append(cnt)
-    torch.cuda.synchronize()
-    nn = nids.cpu().tolist()
-    for g in range(G):
-        assert torch.equal(outs[0][g, : nn[g]], outs[1][g, : nn[g]]), g
-    assert torch.equal(cnts[0][:, :5], cnts[1][:, :5])

@@ -28,7 +28,26 @@ def test_library_exports_every_declared_symbol():
     for name in declared:
         assert hasattr(lib, name), name
     assert declared == set(_lib.exported_symbols())
-    assert lib.rg_abi_version() == 1
+    assert lib.rg_abi_version() == 2
+
+
+def test_library_exports_only_the_c_abi():
+    """The .so's dynamic symbol table is exactly the header's rg_* entry
+    points (version script): the statically linked CUDA runtime stays
+    local, so none of its cuda* entry points is re-exported."""
+    import shutil
+    import subprocess
+
+    from paper_2505_10806_b200 import _lib
+
+    if shutil.which("nm") is None:
+        pytest.skip("nm not available")
+    out = subprocess.run(["nm", "-D", "--defined-only", str(_lib.LIB_PATH)], capture_output=True,
+                         text=True, check=True).stdout
+    names = {ln.split()[-1] for ln in out.splitlines() if ln.strip()}
+    header = (ROOT / "include" / "rapidgnn_b200.h").read_text()
+    declared = set(re.findall(r"^(?:const char\*|int|int64_t)\s+(rg_\w+)\(", header, re.M))
+    assert names == declared, sorted(names ^ declared)
 
 
 def test_philox_matches_numpy():

@@ -167,3 +167,31 @@ def test_mean_aggregation_oracle_in_order():
     exp0 = ((np.float32(0) + h[0]) + h[2] + h[4]) / np.float32(3)
     assert np.array_equal(mean[0], exp0.astype(np.float32))
     assert np.array_equal(hs, h[[1, 3]])
+
+
+def _h16(*arrays) -> str:
+    m = hashlib.blake2b(digest_size=16)
+    for a in arrays:
+        m.update(np.ascontiguousarray(a).tobytes())
+    return m.hexdigest()
+
+
+@pytest.mark.parametrize("name", ["small", "replay", "c1",
+                                  pytest.param("products", marks=pytest.mark.slow)])
+def test_c_oracle_generator_matches_reference(golden, name):
+    """oracle/oracle_graph.c (the bench reference arm's inputs, no product
+    library) reproduces gnnpipe's synth_powerlaw + partition_edgecut: CSR,
+    features and masks hashes, and the LDG owner arrays."""
+    from oracle import graph_oracle as go
+
+    rec = golden["generator"][name]
+    n, m, d, _c, s = rec["args"]
+    g = go.synth_powerlaw(n, m, d, s)
+    want = rec["hash"]
+    assert _h16(g.indptr.astype("<i8")) == want["indptr"]
+    assert _h16(g.indices.astype("<i4")) == want["indices"]
+    assert _h16(g.features.astype("<f4")) == want["features"]
+    assert _h16(g.train_mask.astype("u1"), g.val_mask.astype("u1"),
+                g.test_mask.astype("u1")) == want["masks"]
+    for k, hk in rec["owner"].items():
+        assert _h16(go.partition_edgecut(g, int(k)).astype("<i8")) == hk, k
