@@ -143,14 +143,14 @@ class BlockSampler:
         n = len(seeds)
         if n > self.caps[0]:
             raise ValueError(f"{n} seeds exceed the sampler capacity {self.caps[0]}")
-        host = np.empty(n + 3, dtype=np.int32)
-        host[:n] = seeds
-        host[n] = n
-        host[n + 1:n + 3] = np.array([rng_seed & (2**64 - 1)], dtype=np.uint64).view(np.int32)
+        host = np.empty(n + 3, dtype=np.int32)  # [rng seed (2 words) | count | seeds]
+        host[0:2] = np.array([rng_seed & (2**64 - 1)], dtype=np.uint64).view(np.int32)
+        host[2] = n
+        host[3:] = seeds
         dev = torch.from_numpy(host).to(self.dg.device)
-        self.seeds[b, :n].copy_(dev[:n])
-        self.nseeds[b: b + 1].copy_(dev[n:n + 1])
-        self.rng[b: b + 1].copy_(dev[n + 1:n + 3].view(torch.int64))
+        self.rng[b: b + 1].copy_(dev[0:2].view(torch.int64))
+        self.nseeds[b: b + 1].copy_(dev[2:3])
+        self.seeds[b, :n].copy_(dev[3:])
 
     def run(self, ngroup: int | None = None) -> None:
         """Sample all L levels for slots [0, ngroup) on the current stream."""
