@@ -282,6 +282,139 @@ __global__ void __launch_bounds__(kGatherWarps * 32, 4)
   }
 }
 
+// ---- window-major gather from the input bitmaps ----------------------------
+// The group's input sets as the sampler leaves them: bm[b][w] (bit j of word w
+// = node 32w+j is in batch b's input set) and wpre[b][w] (rank of node 32w in
+// that sorted set).  Work items k = w*G + b — id-window-major: every batch's
+// rows for the same 32 ids are copied around the same time, so each source
+// row is read from HBM about once and then served from L2 to the group's
+// other batches (the rank-major queue above lets batches drift apart in id
+// space by up to ~10^4 ids, far enough that the bundle write stream evicts
+// the shared rows in between: ~5x re-reads at G = 128).  No id list is read:
+// a word's set bits give the ids, its wpre entry the output rank.
+constexpr unsigned kWordClaim = 16;
+
+__global__ void __launch_bounds__(kGatherWarps * 32, 4)
+    gather_window_kernel(const uint32_t* __restrict__ bm, const int32_t* __restrict__ wpre,
+                         int64_t nwords, int G, int64_t cap, const uint32_t* __restrict__ route,
+                         const __grid_constant__ Bases bases, int src_stride, int stride,
+                         int nvec, int dq, int dr, int my_part, uint32_t peer_mask,
+                         float* __restrict__ out, uint32_t* __restrict__ counters,
+                         unsigned* __restrict__ queue) {
+  __shared__ uint32_t s_cnt[kQueueMaxG][RG_NCOUNTERS];
+  __shared__ const float* s_base[16];
+  __shared__ unsigned long long s_src[kGatherWarps][32];
+  const int lane = lane_id();
+  const int warp = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int i = threadIdx.x; i < kQueueMaxG * RG_NCOUNTERS; i += blockDim.x)
+    (&s_cnt[0][0])[i] = 0;
+  if (threadIdx.x < 16) s_base[threadIdx.x] = bases.p[threadIdx.x];
+  __syncthreads();
+  unsigned long long* srcw = s_src[warp];
+  const unsigned items = (unsigned)nwords * (unsigned)G;
+  for (;;) {
+    unsigned t0 = 0;
+    if (lane == 0) t0 = atomicAdd(queue, kWordClaim);
+    t0 = __shfl_sync(kFull, t0, 0);
+    if (t0 >= items) break;
+    // the claim's words and ranks, one item per lane, loaded together
+    const unsigned kl = t0 + lane;
+    uint32_t my_word = 0;
+    int my_base = 0, my_b = 0;
+    int64_t my_w = 0;
+    if (lane < (int)kWordClaim && kl < items) {
+      my_w = kl / (unsigned)G;
+      my_b = (int)(kl - (unsigned)my_w * (unsigned)G);
+      const int64_t at = (int64_t)my_b * nwords + my_w;
+      my_word = __ldg(bm + at);
+      if (my_word) my_base = __ldg(wpre + at);
+    }
+    unsigned todo = __ballot_sync(kFull, my_word != 0u);
+    while (todo) {
+      const int src_lane = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const uint32_t word = __shfl_sync(kFull, my_word, src_lane);
+      const int base = __shfl_sync(kFull, my_base, src_lane);
+      const int b = __shfl_sync(kFull, my_b, src_lane);
+      const int64_t w = __shfl_sync(kFull, my_w, src_lane);
+      const int m = __popc(word);
+      // bit lanes: route, provenance, source address into the row's slot
+      const bool set = (word >> lane) & 1u;
+      uint32_t rt = RG_ROUTE_INVALID;
+      if (set) rt = __ldg(route + (w * 32 + lane));
+      const int kind = (int)(rt >> RG_KIND_SHIFT);
+      const float* bp = (set && rt != RG_ROUTE_INVALID) ? s_base[kind] : nullptr;
+      const bool bad = set && bp == nullptr;
+      const bool local = set && !bad && kind == my_part;
+      const bool hit = set && !bad && kind == (int)RG_KIND_CACHE;
+      const bool fb = set && !bad && !local && !hit;
+      const unsigned n_local = __popc(__ballot_sync(kFull, local));
+      const unsigned n_hit = __popc(__ballot_sync(kFull, hit));
+      const unsigned n_fb = __popc(__ballot_sync(kFull, fb));
+      const unsigned n_bad = __popc(__ballot_sync(kFull, bad));
+      const unsigned n_peer = __popc(__ballot_sync(kFull, fb && ((peer_mask >> kind) & 1u)));
+      const unsigned om = __reduce_or_sync(kFull, fb ? (1u << kind) : 0u);
+      if (lane == 0) {
+        uint32_t* sc = s_cnt[b];
+        if (n_local) atomicAdd(sc + RG_CNT_LOCAL, n_local);
+        if (n_hit) atomicAdd(sc + RG_CNT_HIT, n_hit);
+        if (n_fb) atomicAdd(sc + RG_CNT_FALLBACK, n_fb);
+        if (n_bad) atomicAdd(sc + RG_CNT_BAD, n_bad);
+        if (n_peer) atomicAdd(sc + RG_CNT_PEER, n_peer);
+        if (om) atomicOr(sc + RG_CNT_OWNER_MASK, om);
+      }
+      if (set)
+        srcw[__popc(word & lt)] = reinterpret_cast<unsigned long long>(
+            bp ? bp + (int64_t)(rt & RG_ROW_MASK) * src_stride : nullptr);
+      __syncwarp();
+      float4* dst = reinterpret_cast<float4*>(out + ((int64_t)b * cap + base) * stride);
+      const int total = m * nvec;
+      int er = lane / nvec, ec = lane - (lane / nvec) * nvec;
+      for (int e0 = 0; e0 < total; e0 += 32 * kUnroll) {
+        float4 v[kUnroll];
+        int rr[kUnroll], cc[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          rr[u] = er;
+          cc[u] = ec;
+          ec += dr;
+          er += dq;
+          if (ec >= nvec) {
+            ec -= nvec;
+            ++er;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          const int e = e0 + u * 32 + lane;
+          const unsigned long long sp = e < total ? srcw[rr[u]] : 0ull;
+          v[u] = sp ? ld_stream(reinterpret_cast<const float4*>(sp) + cc[u])
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          const int e = e0 + u * 32 + lane;
+          if (e < total) st_stream(dst + e, v[u]);
+        }
+      }
+      __syncwarp();  // srcw is rewritten by the next word
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < G * RG_NCOUNTERS; i += blockDim.x) {
+    const int b = i / RG_NCOUNTERS, k = i - b * RG_NCOUNTERS;
+    const uint32_t x = s_cnt[b][k];
+    if (x) {
+      uint32_t* g = counters + (int64_t)b * RG_NCOUNTERS + k;
+      if (k == RG_CNT_OWNER_MASK)
+        atomicOr(g, x);
+      else
+        atomicAdd(g, x);
+    }
+  }
+}
+
 // per-device ring of queue counters: one slot per launch (zeroed on the
 // launch stream), so concurrent gathers on different streams never share
 unsigned* queue_slot(cudaStream_t s) {
@@ -389,6 +522,40 @@ extern "C" int rg_gather_bundle(const int32_t* d_ids, const int32_t* d_nids, int
         d_ids, d_nids, cap, d_route, bases, src_stride, stride, nvec, dq, dr, my_part, peer_mask,
         d_out, d_counters);
   return check_launch("gather_bundle");
+}
+
+extern "C" int rg_gather_window(const uint32_t* d_bm, const int32_t* d_wpre, int64_t nwords,
+                                int32_t G, int64_t cap, const uint32_t* d_route,
+                                const float* const* h_bases, int32_t src_stride, int32_t stride,
+                                int32_t my_part, uint32_t peer_mask, float* d_out,
+                                uint32_t* d_counters, void* stream) {
+  RG_REQUIRE(G >= 1 && G <= kQueueMaxG && cap >= 1 && nwords >= 1,
+             "rg_gather_window: bad sizes (G <= %d)", kQueueMaxG);
+  RG_REQUIRE((uint64_t)G * (uint64_t)nwords < (1ull << 32) - kWordClaim,
+             "rg_gather_window: G * nwords above the 32-bit work queue");
+  RG_REQUIRE(stride >= 4 && stride % 4 == 0, "rg_gather_window: stride %d not a multiple of 4",
+             stride);
+  RG_REQUIRE(src_stride >= stride && src_stride % 4 == 0,
+             "rg_gather_window: src_stride %d < stride %d or not a multiple of 4", src_stride,
+             stride);
+  RG_REQUIRE(((uintptr_t)d_out & 15) == 0, "rg_gather_window: output not 16-byte aligned");
+  Bases bases;
+  for (int i = 0; i < 16; ++i) {
+    bases.p[i] = h_bases[i];
+    RG_REQUIRE(((uintptr_t)bases.p[i] & 15) == 0, "rg_gather_window: base %d misaligned", i);
+  }
+  const int nvec = stride / 4;
+  const int dq = 32 / nvec, dr = 32 % nvec;
+  unsigned* q = queue_slot((cudaStream_t)stream);
+  if (!q) return check_launch("gather window queue");
+  static const int env_ctas = [] {
+    const char* e = getenv("RG_GATHER_CTAS_PER_SM");
+    return e ? std::max(1, atoi(e)) : 3;
+  }();
+  gather_window_kernel<<<kNumSMs * env_ctas, kGatherWarps * 32, 0, (cudaStream_t)stream>>>(
+      d_bm, d_wpre, nwords, G, cap, d_route, bases, src_stride, stride, nvec, dq, dr, my_part,
+      peer_mask, d_out, d_counters, q);
+  return check_launch("gather_window");
 }
 
 extern "C" int rg_route_with_cache(const uint32_t* d_base_route, int64_t n, const int32_t* d_hot,

@@ -128,6 +128,9 @@ class BlockSampler:
                     for d in range(self.L)]
         self.cnt = [torch.empty((G, caps[d]), dtype=I32, device=dev) for d in range(self.L)]
         self.bm = torch.empty((G, dg.nwords), dtype=I32, device=dev)
+        # rank of node 32w in each batch's input set (level L): drives the
+        # id-window-major bundle gather (rg_gather_window)
+        self.wpre = torch.empty((G, dg.nwords), dtype=I32, device=dev)
         lib = _lib.device()
         self.chunk = torch.empty((G, int(lib.rg_bitmap_chunks(dg.nwords))), dtype=I32, device=dev)
         self.slow = (torch.empty(1 + G * max(caps[:-1]), dtype=I32, device=dev)
@@ -167,7 +170,8 @@ class BlockSampler:
                       ptr(self.rng), ptr(self.ell[d]), ptr(self.cnt[d]), ptr(self.bm), dg.nwords,
                       ptr(self.slow), ptr(self.meta), int(dg.sorted_rows), self.prng_code, s)
             _lib.call("rg_bitmap_compact", ptr(self.bm), dg.nwords, G, ptr(self.chunk),
-                      ptr(self.front[d + 1]), self.caps[d + 1], ptr(self.nfront[d + 1]), None, s)
+                      ptr(self.front[d + 1]), self.caps[d + 1], ptr(self.nfront[d + 1]),
+                      ptr(self.wpre) if d == self.L - 1 else None, s)
 
     def edges(self, d: int, ngroup: int | None = None):
         """Flat (src, dst) of level d for every slot: (src, dst, nedge) device."""

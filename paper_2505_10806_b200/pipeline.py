@@ -14,6 +14,7 @@ cache fill -> cache route) follows train.py:190-204 / cache.py:80-148.
 
 from __future__ import annotations
 
+import os
 import queue
 import threading
 import time
@@ -79,6 +80,9 @@ class WorkerPipeline:
         self.prefetch = False
         self.pf_transport = "p2p"
         self.timeline: list | None = None  # [(name, slot, start ev, end ev)] when set
+        # "window": id-window-major gather from the input bitmaps (default);
+        # "ids": the rank-major chunk queue over the sorted id lists
+        self.gather_mode = os.environ.get("RG_GATHER_MODE", "window")
 
     # -- group prefetch of peer rows (multi-GPU, rg_prefetch.cu) -------------
     def enable_prefetch(self, transport: str = "p2p", rank: int = 0, world: int = 1) -> None:
@@ -369,11 +373,16 @@ class WorkerPipeline:
             for q, t in self.shadow[slot].items():
                 bases[q] = t.data_ptr()
             peer_mask = 0  # every row is local now
+        cnt = ptr(self.counters) + i0 * _lib.RG_NCOUNTERS * 4
+        if self.gather_mode == "window" and ng <= 128 and peer_mask == 0:
+            # id-window-major, straight from the group's input bitmaps
+            _lib.call("rg_gather_window", ptr(smp.bm), ptr(smp.wpre), self.dg.nwords, ng,
+                      self.cap_in, ptr(route), bases_array(bases), st.src_stride, st.stride,
+                      self.my_part, st.peer_mask, ptr(rows), cnt, _lib.stream_handle())
+            return
         _lib.call("rg_gather_bundle", ptr(smp.front[smp.L]), ptr(smp.nfront[smp.L]), self.cap_in,
                   ng, ptr(route), bases_array(bases), st.src_stride, st.stride,
-                  self.my_part, peer_mask,
-                  ptr(rows), ptr(self.counters) + i0 * _lib.RG_NCOUNTERS * 4,
-                  _lib.stream_handle())
+                  self.my_part, peer_mask, ptr(rows), cnt, _lib.stream_handle())
 
     def totals(self) -> dict:
         """Epoch accounting so far (syncs): provenance sums and fallback
