@@ -290,9 +290,12 @@ __global__ void __launch_bounds__(kGatherWarps * 32, 4)
 // row is read from HBM about once and then served from L2 to the group's
 // other batches (the rank-major queue above lets batches drift apart in id
 // space by up to ~10^4 ids, far enough that the bundle write stream evicts
-// the shared rows in between: ~5x re-reads at G = 128).  No id list is read:
-// a word's set bits give the ids, its wpre entry the output rank.
-constexpr unsigned kWordClaim = 16;
+// the shared rows in between: DRAM reads 5.2 GB per G = 128 launch against
+// 2.5 GB here).  No id list is read: a window's set bits give the ids, its
+// wpre entry the output rank of its first row.  Items are windows of
+// kWinWords words (128 ids, ~34 rows at Products density) of one batch.
+constexpr int kWinWords = 4;  // item = 4 bitmap words (128 ids) of one batch
+constexpr unsigned kWordClaim = 4;
 
 __global__ void __launch_bounds__(kGatherWarps * 32, 4)
     gather_window_kernel(const uint32_t* __restrict__ bm, const int32_t* __restrict__ wpre,
@@ -303,7 +306,7 @@ __global__ void __launch_bounds__(kGatherWarps * 32, 4)
                          unsigned* __restrict__ queue) {
   __shared__ uint32_t s_cnt[kQueueMaxG][RG_NCOUNTERS];
   __shared__ const float* s_base[16];
-  __shared__ unsigned long long s_src[kGatherWarps][32];
+  __shared__ unsigned long long s_src[kGatherWarps][32 * kWinWords];
   const int lane = lane_id();
   const int warp = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
@@ -312,49 +315,64 @@ __global__ void __launch_bounds__(kGatherWarps * 32, 4)
   if (threadIdx.x < 16) s_base[threadIdx.x] = bases.p[threadIdx.x];
   __syncthreads();
   unsigned long long* srcw = s_src[warp];
-  const unsigned items = (unsigned)nwords * (unsigned)G;
+  const int64_t nwin = (nwords + kWinWords - 1) / kWinWords;
+  const unsigned items = (unsigned)nwin * (unsigned)G;
   for (;;) {
     unsigned t0 = 0;
     if (lane == 0) t0 = atomicAdd(queue, kWordClaim);
     t0 = __shfl_sync(kFull, t0, 0);
     if (t0 >= items) break;
-    // the claim's words and ranks, one item per lane, loaded together
-    const unsigned kl = t0 + lane;
-    uint32_t my_word = 0;
-    int my_base = 0, my_b = 0;
-    int64_t my_w = 0;
-    if (lane < (int)kWordClaim && kl < items) {
-      my_w = kl / (unsigned)G;
-      my_b = (int)(kl - (unsigned)my_w * (unsigned)G);
-      const int64_t at = (int64_t)my_b * nwords + my_w;
-      my_word = __ldg(bm + at);
-      if (my_word) my_base = __ldg(wpre + at);
-    }
-    unsigned todo = __ballot_sync(kFull, my_word != 0u);
-    while (todo) {
-      const int src_lane = __ffs(todo) - 1;
-      todo &= todo - 1;
-      const uint32_t word = __shfl_sync(kFull, my_word, src_lane);
-      const int base = __shfl_sync(kFull, my_base, src_lane);
-      const int b = __shfl_sync(kFull, my_b, src_lane);
-      const int64_t w = __shfl_sync(kFull, my_w, src_lane);
-      const int m = __popc(word);
+    int64_t win = t0 / (unsigned)G;  // one division per claim
+    int b = (int)(t0 - (unsigned)win * (unsigned)G) - 1;
+#pragma unroll 1
+    for (unsigned k = t0; k < t0 + kWordClaim && k < items; ++k) {
+      if (++b == G) {
+        b = 0;
+        ++win;
+      }
+      // the window's words (lanes 0..3) and their exclusive bit prefix
+      const int64_t w0 = win * kWinWords;
+      const int64_t wl = w0 + lane;
+      const uint32_t wd = (lane < kWinWords && wl < nwords) ? __ldg(bm + (int64_t)b * nwords + wl)
+                                                           : 0u;
+      int pre = __popc(wd);
+#pragma unroll
+      for (int o = 1; o < kWinWords; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, pre, o);
+        if (lane >= o) pre += y;
+      }
+      const int m = __shfl_sync(kFull, pre, kWinWords - 1);
+      if (m == 0) continue;
+      pre -= __popc(wd);  // exclusive
+      const int base = __ldg(wpre + (int64_t)b * nwords + w0);
       // bit lanes: route, provenance, source address into the row's slot
-      const bool set = (word >> lane) & 1u;
-      uint32_t rt = RG_ROUTE_INVALID;
-      if (set) rt = __ldg(route + (w * 32 + lane));
-      const int kind = (int)(rt >> RG_KIND_SHIFT);
-      const float* bp = (set && rt != RG_ROUTE_INVALID) ? s_base[kind] : nullptr;
-      const bool bad = set && bp == nullptr;
-      const bool local = set && !bad && kind == my_part;
-      const bool hit = set && !bad && kind == (int)RG_KIND_CACHE;
-      const bool fb = set && !bad && !local && !hit;
-      const unsigned n_local = __popc(__ballot_sync(kFull, local));
-      const unsigned n_hit = __popc(__ballot_sync(kFull, hit));
-      const unsigned n_fb = __popc(__ballot_sync(kFull, fb));
-      const unsigned n_bad = __popc(__ballot_sync(kFull, bad));
-      const unsigned n_peer = __popc(__ballot_sync(kFull, fb && ((peer_mask >> kind) & 1u)));
-      const unsigned om = __reduce_or_sync(kFull, fb ? (1u << kind) : 0u);
+      uint32_t rt[kWinWords], word[kWinWords];
+#pragma unroll
+      for (int q = 0; q < kWinWords; ++q) {
+        word[q] = __shfl_sync(kFull, wd, q);
+        rt[q] = ((word[q] >> lane) & 1u) ? __ldg(route + ((w0 + q) * 32 + lane)) : RG_ROUTE_INVALID;
+      }
+      unsigned n_local = 0, n_hit = 0, n_fb = 0, n_bad = 0, n_peer = 0, om = 0;
+#pragma unroll
+      for (int q = 0; q < kWinWords; ++q) {
+        const bool set = (word[q] >> lane) & 1u;
+        const int kind = (int)(rt[q] >> RG_KIND_SHIFT);
+        const float* bp = (set && rt[q] != RG_ROUTE_INVALID) ? s_base[kind] : nullptr;
+        const bool bad = set && bp == nullptr;
+        const bool local = set && !bad && kind == my_part;
+        const bool hit = set && !bad && kind == (int)RG_KIND_CACHE;
+        const bool fb = set && !bad && !local && !hit;
+        n_local += __popc(__ballot_sync(kFull, local));
+        n_hit += __popc(__ballot_sync(kFull, hit));
+        n_fb += __popc(__ballot_sync(kFull, fb));
+        n_bad += __popc(__ballot_sync(kFull, bad));
+        n_peer += __popc(__ballot_sync(kFull, fb && ((peer_mask >> kind) & 1u)));
+        om |= __reduce_or_sync(kFull, fb ? (1u << kind) : 0u);
+        const int off = __shfl_sync(kFull, pre, q);
+        if (set)
+          srcw[off + __popc(word[q] & lt)] = reinterpret_cast<unsigned long long>(
+              bp ? bp + (int64_t)(rt[q] & RG_ROW_MASK) * src_stride : nullptr);
+      }
       if (lane == 0) {
         uint32_t* sc = s_cnt[b];
         if (n_local) atomicAdd(sc + RG_CNT_LOCAL, n_local);
@@ -364,9 +382,6 @@ __global__ void __launch_bounds__(kGatherWarps * 32, 4)
         if (n_peer) atomicAdd(sc + RG_CNT_PEER, n_peer);
         if (om) atomicOr(sc + RG_CNT_OWNER_MASK, om);
       }
-      if (set)
-        srcw[__popc(word & lt)] = reinterpret_cast<unsigned long long>(
-            bp ? bp + (int64_t)(rt & RG_ROW_MASK) * src_stride : nullptr);
       __syncwarp();
       float4* dst = reinterpret_cast<float4*>(out + ((int64_t)b * cap + base) * stride);
       const int total = m * nvec;
@@ -398,15 +413,15 @@ __global__ void __launch_bounds__(kGatherWarps * 32, 4)
           if (e < total) st_stream(dst + e, v[u]);
         }
       }
-      __syncwarp();  // srcw is rewritten by the next word
+      __syncwarp();  // srcw is rewritten by the next item
     }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < G * RG_NCOUNTERS; i += blockDim.x) {
-    const int b = i / RG_NCOUNTERS, k = i - b * RG_NCOUNTERS;
-    const uint32_t x = s_cnt[b][k];
+    const int bb = i / RG_NCOUNTERS, k = i - bb * RG_NCOUNTERS;
+    const uint32_t x = s_cnt[bb][k];
     if (x) {
-      uint32_t* g = counters + (int64_t)b * RG_NCOUNTERS + k;
+      uint32_t* g = counters + (int64_t)bb * RG_NCOUNTERS + k;
       if (k == RG_CNT_OWNER_MASK)
         atomicOr(g, x);
       else
@@ -548,9 +563,13 @@ extern "C" int rg_gather_window(const uint32_t* d_bm, const int32_t* d_wpre, int
   const int dq = 32 / nvec, dr = 32 % nvec;
   unsigned* q = queue_slot((cudaStream_t)stream);
   if (!q) return check_launch("gather window queue");
+  // 4 CTAs/SM (58 registers: the whole register file): gather alone 6.51 ms
+  // at 3 or 4 per SM (Products G = 128), but at 4 no sampler CTA of the next
+  // group can co-reside, and co-running measured slower than back to back
+  // (step 9.88 ms at 4/SM vs 11.23 ms at 3/SM)
   static const int env_ctas = [] {
     const char* e = getenv("RG_GATHER_CTAS_PER_SM");
-    return e ? std::max(1, atoi(e)) : 3;
+    return e ? std::max(1, atoi(e)) : 4;
   }();
   gather_window_kernel<<<kNumSMs * env_ctas, kGatherWarps * 32, 0, (cudaStream_t)stream>>>(
       d_bm, d_wpre, nwords, G, cap, d_route, bases, src_stride, stride, nvec, dq, dr, my_part,
