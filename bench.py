@@ -509,7 +509,6 @@ def main():
         pipe.gather(ng, i0)
         if timed_events is not None:
             timed_events[1].record()
-            unions.add(smp, ng)
         return i0, ng
 
     unions = UnionCounter(dg.nwords)
@@ -569,6 +568,12 @@ def main():
         pipe.timeline = None
     if args.serial and not args.graphs:
         gather_ms = sum(a.elapsed_time(b) for a, b in gev)
+        for kk in range(args.steps):  # distinct rows per launch, outside the timing
+            i0 = ((args.warmup + kk) % n_full) * G
+            ng = min(G, nb - i0)
+            pipe.plan.fill(pipe.perm, 0, i0, ng)
+            smp.run(ng)
+            unions.add(smp, ng)
     else:
         # overlapped run: time the gather alone on the same batches (serial),
         # and the group prefetch (NVLink) on its own

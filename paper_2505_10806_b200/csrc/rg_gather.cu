@@ -430,6 +430,190 @@ __global__ void __launch_bounds__(kGatherWarps * 32, 4)
   }
 }
 
+// ---- staged union gather: each source row read once per group -------------
+// The window kernel above still moves every bundle row through L2 twice (the
+// source read — an L2 hit for all but the first batch — and the write):
+// 68.8 GB of L2 traffic per G = 128 Products launch, near the full-chip L2
+// slice throughput, while the bundle writes alone (34.4 GB) need ~4.6 ms at
+// the measured write-only HBM rate (7.5 TB/s, tools/hbm_probe.py).  Here a
+// CTA owns a window of 32*kW ids for ALL G batches: phase 1 stages every
+// present source row of the window in shared memory (each row read from
+// HBM once per group); phase 2 writes, batch by batch, that batch's rows of
+// the window as one contiguous run (ranks wpre[b][w0] ..).  (A warp-per-id
+// scatter — each row stored straight to every batch holding it — reads once
+// too but scatters 400-B writes over all G bundles at once and measured
+// 11.7 ms: HBM write locality matters more than the reads.)
+template <int kW>
+__global__ void __launch_bounds__(kGatherWarps * 32)
+    gather_staged_kernel(const uint32_t* __restrict__ bm, const int32_t* __restrict__ wpre,
+                         int64_t nwords, int G, int64_t cap, const uint32_t* __restrict__ route,
+                         const __grid_constant__ Bases bases, int src_stride, int stride,
+                         int nvec, int dq, int dr, int my_part, uint32_t peer_mask,
+                         float* __restrict__ out, uint32_t* __restrict__ counters,
+                         unsigned* __restrict__ queue) {
+  constexpr int kIds = 32 * kW;
+  extern __shared__ float4 s_rows[];  // [kIds][nvec]
+  __shared__ uint32_t s_cnt[kQueueMaxG][RG_NCOUNTERS];
+  __shared__ const float* s_base[16];
+  __shared__ unsigned long long s_src[kIds];
+  __shared__ uint32_t s_present[kW], s_mloc[kW], s_mhit[kW], s_mfb[kW], s_mbad[kW], s_mpeer[kW];
+  __shared__ uint32_t s_mq[16][kW];  // fallback ids per owner kind
+  __shared__ uint32_t s_fbkinds;
+  __shared__ uint8_t s_list[kGatherWarps][kIds];  // a batch's rows -> window offsets
+  __shared__ unsigned s_win;
+  const int lane = lane_id(), warp = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int i = threadIdx.x; i < kQueueMaxG * RG_NCOUNTERS; i += blockDim.x)
+    (&s_cnt[0][0])[i] = 0;
+  if (threadIdx.x < 16) s_base[threadIdx.x] = bases.p[threadIdx.x];
+  const int64_t nwin = (nwords + kW - 1) / kW;
+  for (;;) {
+    __syncthreads();  // previous window fully written out; counters zeroed
+    if (threadIdx.x == 0) s_win = atomicAdd(queue, 1u);
+    if (threadIdx.x < kW) s_present[threadIdx.x] = 0;
+    if (threadIdx.x < 16 * kW) (&s_mq[0][0])[threadIdx.x] = 0;
+    if (threadIdx.x == 0) s_fbkinds = 0;
+    __syncthreads();
+    const int64_t win = s_win;
+    if (win >= nwin) break;
+    const int64_t w0 = win * kW;
+    // phase 1a: union of the window over the group's batches
+    for (int i = threadIdx.x; i < G * kW; i += blockDim.x) {
+      const int bb = i / kW, q = i - bb * kW;
+      if (w0 + q < nwords) {
+        const uint32_t x = __ldg(bm + (int64_t)bb * nwords + w0 + q);
+        if (x) atomicOr(&s_present[q], x);
+      }
+    }
+    __syncthreads();
+    // phase 1b: route / kind / source address per id (warp q <-> word q)
+    if (warp < kW) {
+      const uint32_t pres = s_present[warp];
+      const bool here = (pres >> lane) & 1u;
+      const int64_t id = (w0 + warp) * 32 + lane;
+      const uint32_t rt = here ? __ldg(route + id) : RG_ROUTE_INVALID;
+      const int kind = (int)(rt >> RG_KIND_SHIFT);
+      const float* bp = (here && rt != RG_ROUTE_INVALID) ? s_base[kind] : nullptr;
+      const bool bad = here && bp == nullptr;
+      const bool local = here && !bad && kind == my_part;
+      const bool hit = here && !bad && kind == (int)RG_KIND_CACHE;
+      const bool fb = here && !bad && !local && !hit;
+      const unsigned mfb = __ballot_sync(kFull, fb);
+      const unsigned mloc = __ballot_sync(kFull, local), mhit = __ballot_sync(kFull, hit);
+      const unsigned mbad = __ballot_sync(kFull, bad);
+      const unsigned mpeer = __ballot_sync(kFull, fb && ((peer_mask >> kind) & 1u));
+      if (lane == 0) {
+        s_mloc[warp] = mloc;
+        s_mhit[warp] = mhit;
+        s_mfb[warp] = mfb;
+        s_mbad[warp] = mbad;
+        s_mpeer[warp] = mpeer;
+      }
+      if (fb) atomicOr(&s_mq[kind][warp], 1u << lane);
+      const unsigned kinds = __reduce_or_sync(kFull, fb ? (1u << kind) : 0u);
+      s_src[warp * 32 + lane] = reinterpret_cast<unsigned long long>(
+          bp ? bp + (int64_t)(rt & RG_ROW_MASK) * src_stride : nullptr);
+      if (lane == 0 && kinds) atomicOr(&s_fbkinds, kinds);
+    }
+    __syncthreads();
+    // phase 1c: stage the present rows (flattened over ids x vectors)
+    {
+      const int total = kIds * nvec;
+      for (int e = threadIdx.x; e < total; e += blockDim.x) {
+        const int r = e / nvec, c = e - r * nvec;
+        const unsigned long long sp = s_src[r];
+        if (sp) s_rows[e] = ld_stream(reinterpret_cast<const float4*>(sp) + c);
+        else if ((s_present[r >> 5] >> (r & 31)) & 1u) s_rows[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+    __syncthreads();
+    // phase 2: each batch's run of the window, contiguous
+    uint8_t* list = s_list[warp];
+    const uint32_t fbk = s_fbkinds;
+    for (int bb = warp; bb < G; bb += kGatherWarps) {
+      uint32_t wd = 0;
+      if (lane < kW && w0 + lane < nwords) wd = __ldg(bm + (int64_t)bb * nwords + w0 + lane);
+      int pre = __popc(wd);
+#pragma unroll
+      for (int o = 1; o < kW; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, pre, o);
+        if (lane >= o) pre += y;
+      }
+      const int m = __shfl_sync(kFull, pre, kW - 1);
+      if (m == 0) continue;
+      pre -= __popc(wd);
+      const int base = __ldg(wpre + (int64_t)bb * nwords + w0);
+      unsigned n_loc = 0, n_hit = 0, n_fb = 0, n_bad = 0, n_peer = 0, om = 0;
+#pragma unroll
+      for (int q = 0; q < kW; ++q) {
+        const uint32_t word = __shfl_sync(kFull, wd, q);
+        const int off = __shfl_sync(kFull, pre, q);
+        if ((word >> lane) & 1u) list[off + __popc(word & lt)] = (uint8_t)(q * 32 + lane);
+        n_loc += __popc(word & s_mloc[q]);
+        n_hit += __popc(word & s_mhit[q]);
+        n_fb += __popc(word & s_mfb[q]);
+        n_bad += __popc(word & s_mbad[q]);
+        n_peer += __popc(word & s_mpeer[q]);
+        for (unsigned kk = fbk; kk; kk &= kk - 1) {
+          const int kq = __ffs(kk) - 1;
+          if (word & s_mq[kq][q]) om |= 1u << kq;
+        }
+      }
+      if (lane == 0) {
+        uint32_t* sc = s_cnt[bb];
+        if (n_loc) atomicAdd(sc + RG_CNT_LOCAL, n_loc);
+        if (n_hit) atomicAdd(sc + RG_CNT_HIT, n_hit);
+        if (n_fb) atomicAdd(sc + RG_CNT_FALLBACK, n_fb);
+        if (n_bad) atomicAdd(sc + RG_CNT_BAD, n_bad);
+        if (n_peer) atomicAdd(sc + RG_CNT_PEER, n_peer);
+        if (om) atomicOr(sc + RG_CNT_OWNER_MASK, om);
+      }
+      __syncwarp();
+      float4* dst = reinterpret_cast<float4*>(out + ((int64_t)bb * cap + base) * stride);
+      const int total = m * nvec;
+      int er = lane / nvec, ec = lane - (lane / nvec) * nvec;
+      for (int e0 = 0; e0 < total; e0 += 32 * kUnroll) {
+        float4 v[kUnroll];
+        int rr[kUnroll], cc[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          rr[u] = er;
+          cc[u] = ec;
+          ec += dr;
+          er += dq;
+          if (ec >= nvec) {
+            ec -= nvec;
+            ++er;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          const int e = e0 + u * 32 + lane;
+          if (e < total) v[u] = s_rows[(int)list[rr[u]] * nvec + cc[u]];
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          const int e = e0 + u * 32 + lane;
+          if (e < total) st_stream(dst + e, v[u]);
+        }
+      }
+      __syncwarp();  // list is rebuilt for the warp's next batch
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < G * RG_NCOUNTERS; i += blockDim.x) {
+    const int bb = i / RG_NCOUNTERS, k = i - bb * RG_NCOUNTERS;
+    const uint32_t x = s_cnt[bb][k];
+    if (x) {
+      uint32_t* g = counters + (int64_t)bb * RG_NCOUNTERS + k;
+      if (k == RG_CNT_OWNER_MASK)
+        atomicOr(g, x);
+      else
+        atomicAdd(g, x);
+    }
+  }
+}
+
 // per-device ring of queue counters: one slot per launch (zeroed on the
 // launch stream), so concurrent gathers on different streams never share
 unsigned* queue_slot(cudaStream_t s) {
@@ -571,6 +755,37 @@ extern "C" int rg_gather_window(const uint32_t* d_bm, const int32_t* d_wpre, int
     const char* e = getenv("RG_GATHER_CTAS_PER_SM");
     return e ? std::max(1, atoi(e)) : 4;
   }();
+  static const int kernel = [] {  // 1: staged union (default), 0: window-major
+    const char* e = getenv("RG_GATHER_UNION");
+    return e ? atoi(e) : 1;
+  }();
+  // staged rows per CTA <= ~56 KB: 4 CTAs per SM at Products (128 ids x 400 B)
+  static const int kw_max = [] {
+    const char* e = getenv("RG_GATHER_KW");
+    return e ? std::max(1, std::min(4, atoi(e))) : 2;  // 2: 5.96 ms, 4: 5.97, 1: 6.79
+  }();
+  int kw = kw_max;
+  while (kw > 1 && (int64_t)32 * kw * nvec * 16 > 56 * 1024) kw >>= 1;
+  const size_t srows = (size_t)32 * kw * nvec * 16;
+  if (kernel && srows <= 200 * 1024) {
+    cudaStream_t st = (cudaStream_t)stream;
+    auto go = [&](auto kern) {
+      static bool attr = false;  // per instantiation
+      if (!attr) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+      }
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kGatherWarps * 32, srows);
+      kern<<<kNumSMs * std::max(1, per_sm), kGatherWarps * 32, srows, st>>>(
+          d_bm, d_wpre, nwords, G, cap, d_route, bases, src_stride, stride, nvec, dq, dr, my_part,
+          peer_mask, d_out, d_counters, q);
+      return check_launch("gather_staged");
+    };
+    if (kw == 4) return go(gather_staged_kernel<4>);
+    if (kw == 2) return go(gather_staged_kernel<2>);
+    return go(gather_staged_kernel<1>);
+  }
   gather_window_kernel<<<kNumSMs * env_ctas, kGatherWarps * 32, 0, (cudaStream_t)stream>>>(
       d_bm, d_wpre, nwords, G, cap, d_route, bases, src_stride, stride, nvec, dq, dr, my_part,
       peer_mask, d_out, d_counters, q);
