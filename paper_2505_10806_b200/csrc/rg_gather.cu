@@ -777,6 +777,11 @@ extern "C" int rg_gather_window(const uint32_t* d_bm, const int32_t* d_wpre, int
       }
       int per_sm = 0;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kGatherWarps * 32, srows);
+      static const int cap_sm = [] {
+        const char* e = getenv("RG_GATHER_STAGED_CTAS");
+        return e ? std::max(1, atoi(e)) : 0;
+      }();
+      if (cap_sm) per_sm = std::min(per_sm, cap_sm);
       kern<<<kNumSMs * std::max(1, per_sm), kGatherWarps * 32, srows, st>>>(
           d_bm, d_wpre, nwords, G, cap, d_route, bases, src_stride, stride, nvec, dq, dr, my_part,
           peer_mask, d_out, d_counters, q);
