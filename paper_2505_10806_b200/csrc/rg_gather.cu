@@ -459,7 +459,8 @@ __global__ void __launch_bounds__(kGatherWarps * 32)
   __shared__ uint32_t s_present[kW], s_mloc[kW], s_mhit[kW], s_mfb[kW], s_mbad[kW], s_mpeer[kW];
   __shared__ uint32_t s_mq[16][kW];  // fallback ids per owner kind
   __shared__ uint32_t s_fbkinds;
-  __shared__ uint8_t s_list[kGatherWarps][kIds];  // a batch's rows -> window offsets
+  __shared__ uint32_t s_words[kQueueMaxG * kW];  // bm[b][w0 + q] of every batch
+  __shared__ int32_t s_rbase[kQueueMaxG];         // wpre[b][w0]
   __shared__ unsigned s_win;
   const int lane = lane_id(), warp = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
@@ -477,14 +478,16 @@ __global__ void __launch_bounds__(kGatherWarps * 32)
     const int64_t win = s_win;
     if (win >= nwin) break;
     const int64_t w0 = win * kW;
-    // phase 1a: union of the window over the group's batches
+    // phase 1a: the group's words of the window (kept for phase 2), their
+    // union, and every batch's rank base
     for (int i = threadIdx.x; i < G * kW; i += blockDim.x) {
       const int bb = i / kW, q = i - bb * kW;
-      if (w0 + q < nwords) {
-        const uint32_t x = __ldg(bm + (int64_t)bb * nwords + w0 + q);
-        if (x) atomicOr(&s_present[q], x);
-      }
+      uint32_t x = 0;
+      if (w0 + q < nwords) x = __ldg(bm + (int64_t)bb * nwords + w0 + q);
+      s_words[i] = x;
+      if (x) atomicOr(&s_present[q], x);
     }
+    for (int bb = threadIdx.x; bb < G; bb += blockDim.x) s_rbase[bb] = __ldg(wpre + (int64_t)bb * nwords + w0);
     __syncthreads();
     // phase 1b: route / kind / source address per id (warp q <-> word q)
     if (warp < kW) {
@@ -516,23 +519,30 @@ __global__ void __launch_bounds__(kGatherWarps * 32)
       if (lane == 0 && kinds) atomicOr(&s_fbkinds, kinds);
     }
     __syncthreads();
-    // phase 1c: stage the present rows (flattened over ids x vectors)
+    // phase 1c: stage the present rows; warp w copies ids 4w.. (row-aligned:
+    // lane c moves vector c, four rows' loads in flight per lane)
     {
-      const int total = kIds * nvec;
-      for (int e = threadIdx.x; e < total; e += blockDim.x) {
-        const int r = e / nvec, c = e - r * nvec;
-        const unsigned long long sp = s_src[r];
-        if (sp) s_rows[e] = ld_stream(reinterpret_cast<const float4*>(sp) + c);
-        else if ((s_present[r >> 5] >> (r & 31)) & 1u) s_rows[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+      constexpr int kR = 4;
+      for (int r0 = warp * kR; r0 < kIds; r0 += kGatherWarps * kR) {
+        unsigned long long sp[kR];
+#pragma unroll
+        for (int u = 0; u < kR; ++u) sp[u] = s_src[r0 + u];
+        for (int c = lane; c < nvec; c += 32) {
+          float4 v[kR];
+#pragma unroll
+          for (int u = 0; u < kR; ++u)
+            v[u] = sp[u] ? ld_stream(reinterpret_cast<const float4*>(sp[u]) + c)
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int u = 0; u < kR; ++u) s_rows[(r0 + u) * nvec + c] = v[u];
+        }
       }
     }
     __syncthreads();
     // phase 2: each batch's run of the window, contiguous
-    uint8_t* list = s_list[warp];
     const uint32_t fbk = s_fbkinds;
     for (int bb = warp; bb < G; bb += kGatherWarps) {
-      uint32_t wd = 0;
-      if (lane < kW && w0 + lane < nwords) wd = __ldg(bm + (int64_t)bb * nwords + w0 + lane);
+      const uint32_t wd = lane < kW ? s_words[bb * kW + lane] : 0u;
       int pre = __popc(wd);
 #pragma unroll
       for (int o = 1; o < kW; o <<= 1) {
@@ -542,13 +552,11 @@ __global__ void __launch_bounds__(kGatherWarps * 32)
       const int m = __shfl_sync(kFull, pre, kW - 1);
       if (m == 0) continue;
       pre -= __popc(wd);
-      const int base = __ldg(wpre + (int64_t)bb * nwords + w0);
+      const int base = s_rbase[bb];
       unsigned n_loc = 0, n_hit = 0, n_fb = 0, n_bad = 0, n_peer = 0, om = 0;
 #pragma unroll
       for (int q = 0; q < kW; ++q) {
         const uint32_t word = __shfl_sync(kFull, wd, q);
-        const int off = __shfl_sync(kFull, pre, q);
-        if ((word >> lane) & 1u) list[off + __popc(word & lt)] = (uint8_t)(q * 32 + lane);
         n_loc += __popc(word & s_mloc[q]);
         n_hit += __popc(word & s_mhit[q]);
         n_fb += __popc(word & s_mfb[q]);
@@ -569,35 +577,32 @@ __global__ void __launch_bounds__(kGatherWarps * 32)
         if (om) atomicOr(sc + RG_CNT_OWNER_MASK, om);
       }
       __syncwarp();
+      // the batch's rows in id order = consecutive output rows; four rows per
+      // step, lane c moves vector c of each (no per-element index math)
       float4* dst = reinterpret_cast<float4*>(out + ((int64_t)bb * cap + base) * stride);
-      const int total = m * nvec;
-      int er = lane / nvec, ec = lane - (lane / nvec) * nvec;
-      for (int e0 = 0; e0 < total; e0 += 32 * kUnroll) {
-        float4 v[kUnroll];
-        int rr[kUnroll], cc[kUnroll];
+      int k = 0;
+#pragma unroll 1
+      for (int q = 0; q < kW; ++q) {
+        uint32_t word = __shfl_sync(kFull, wd, q);
+        while (word) {
+          int j[4];
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          rr[u] = er;
-          cc[u] = ec;
-          ec += dr;
-          er += dq;
-          if (ec >= nvec) {
-            ec -= nvec;
-            ++er;
+          for (int u = 0; u < 4; ++u) {
+            j[u] = word ? q * 32 + __ffs(word) - 1 : -1;
+            word &= word - 1;
           }
-        }
+          for (int c = lane; c < nvec; c += 32) {
+            float4 v[4];
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          const int e = e0 + u * 32 + lane;
-          if (e < total) v[u] = s_rows[(int)list[rr[u]] * nvec + cc[u]];
-        }
+            for (int u = 0; u < 4; ++u)
+              if (j[u] >= 0) v[u] = s_rows[j[u] * nvec + c];
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          const int e = e0 + u * 32 + lane;
-          if (e < total) st_stream(dst + e, v[u]);
+            for (int u = 0; u < 4; ++u)
+              if (j[u] >= 0) st_stream(dst + (int64_t)(k + u) * nvec + c, v[u]);
+          }
+          k += (j[0] >= 0) + (j[1] >= 0) + (j[2] >= 0) + (j[3] >= 0);
         }
       }
-      __syncwarp();  // list is rebuilt for the warp's next batch
     }
   }
   __syncthreads();

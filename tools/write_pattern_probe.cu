@@ -10,6 +10,17 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// incompressible payload (the bundle rows are random floats; B200's L2 tries
+// to compress every written sector, and constant data would compress)
+__device__ __forceinline__ float4 noise(int64_t i) {
+  uint64_t x = (uint64_t)i * 0x9E3779B97F4A7C15ull;
+  x ^= x >> 31;
+  x *= 0xBF58476D1CE4E5B9ull;
+  x ^= x >> 29;
+  return make_float4(__uint_as_float((uint32_t)x), __uint_as_float((uint32_t)(x >> 32)),
+                     __uint_as_float((uint32_t)(x >> 7)), __uint_as_float((uint32_t)(x >> 19)));
+}
+
 __global__ void runs_kernel(float4* out, int64_t region_vec, int G, int run_vec, int64_t nwin,
                             unsigned* queue) {
   __shared__ unsigned s_w;
@@ -22,7 +33,7 @@ __global__ void runs_kernel(float4* out, int64_t region_vec, int G, int run_vec,
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int b = warp; b < G; b += blockDim.x >> 5) {
       float4* dst = out + (int64_t)b * region_vec + w * run_vec;
-      for (int e = lane; e < run_vec; e += 32) dst[e] = make_float4(1.f, 2.f, 3.f, 4.f);
+      for (int e = lane; e < run_vec; e += 32) dst[e] = noise(w * run_vec + e + b);
     }
   }
 }
@@ -30,7 +41,7 @@ __global__ void runs_kernel(float4* out, int64_t region_vec, int G, int run_vec,
 __global__ void seq_kernel(float4* out, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = make_float4(1.f, 2.f, 3.f, 4.f);
+    out[i] = noise(i);
 }
 
 int main() {
