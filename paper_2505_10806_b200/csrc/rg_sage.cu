@@ -61,21 +61,20 @@ struct alignas(sizeof(T) * N) Vec {
 };
 
 // A group of SW lanes owns one output row; lane j of the group handles the
-// row's vectors j, j + SW, ... (up to kVPL per pass over the columns).
-constexpr int kVPL = 4;
-
-template <typename T, int N>
+// row's vectors j, j + SW, ... (up to V per pass over the columns; V is
+// chosen per launch as ceil(nvec / SW), so registers match the row width).
+template <typename T, int N, int V>
 __device__ __forceinline__ void load_vecs(const T* __restrict__ row, int nvec, int j0, int SW,
-                                          Vec<T, N> (&x)[kVPL]) {
+                                          Vec<T, N> (&x)[V]) {
 #pragma unroll
-  for (int u = 0; u < kVPL; ++u) {
+  for (int u = 0; u < V; ++u) {
     const int vi = j0 + u * SW;
     if (vi < nvec) x[u] = *reinterpret_cast<const Vec<T, N>*>(row + (int64_t)vi * N);
   }
 }
 
 // mean[t] = (((0 + h[p_1]) + h[p_2]) + ...) / max(cnt_t, 1); self[t] = h[self_pos[t]]
-template <typename T, int N>
+template <typename T, int N, int V>
 __global__ void __launch_bounds__(kWarps * 32)
     sage_fwd_kernel(const T* __restrict__ h, int ldh, int H, const int32_t* __restrict__ epos,
                     const int32_t* __restrict__ self_pos, int64_t n_dst,
@@ -92,35 +91,39 @@ __global__ void __launch_bounds__(kWarps * 32)
     const T denom = (T)max(c, 1);
     const int32_t* ep = epos + t * F;
     const int ps = __ldg(self_pos + t);
-    for (int vb = 0; vb < nvec; vb += SW * kVPL) {
+    for (int vb = 0; vb < nvec; vb += SW * V) {
       const int jb = vb + j0;
-      Vec<T, N> acc[kVPL];
+      Vec<T, N> acc[V];
 #pragma unroll
-      for (int u = 0; u < kVPL; ++u)
+      for (int u = 0; u < V; ++u)
 #pragma unroll
         for (int k = 0; k < N; ++k) acc[u].v[k] = (T)0;
+      constexpr int R = V == 1 ? 4 : 2;  // rows' loads in flight; adds stay in edge order
       int r = 0;
-      for (; r + 2 <= c; r += 2) {  // two rows' loads in flight, adds in edge order
-        Vec<T, N> x0[kVPL], x1[kVPL];
-        load_vecs<T, N>(h + (int64_t)__ldg(ep + r) * ldh, nvec, jb, SW, x0);
-        load_vecs<T, N>(h + (int64_t)__ldg(ep + r + 1) * ldh, nvec, jb, SW, x1);
+      for (; r + R <= c; r += R) {
+        Vec<T, N> x[R][V];
 #pragma unroll
-        for (int u = 0; u < kVPL; ++u)
+        for (int q = 0; q < R; ++q)
+          load_vecs<T, N, V>(h + (int64_t)__ldg(ep + r + q) * ldh, nvec, jb, SW, x[q]);
 #pragma unroll
-          for (int k = 0; k < N; ++k) acc[u].v[k] = (acc[u].v[k] + x0[u].v[k]) + x1[u].v[k];
+        for (int q = 0; q < R; ++q)
+#pragma unroll
+          for (int u = 0; u < V; ++u)
+#pragma unroll
+            for (int k = 0; k < N; ++k) acc[u].v[k] += x[q][u].v[k];
       }
-      if (r < c) {
-        Vec<T, N> x0[kVPL];
-        load_vecs<T, N>(h + (int64_t)__ldg(ep + r) * ldh, nvec, jb, SW, x0);
+      for (; r < c; ++r) {
+        Vec<T, N> x0[V];
+        load_vecs<T, N, V>(h + (int64_t)__ldg(ep + r) * ldh, nvec, jb, SW, x0);
 #pragma unroll
-        for (int u = 0; u < kVPL; ++u)
+        for (int u = 0; u < V; ++u)
 #pragma unroll
           for (int k = 0; k < N; ++k) acc[u].v[k] += x0[u].v[k];
       }
-      Vec<T, N> sv[kVPL];
-      if (self) load_vecs<T, N>(h + (int64_t)ps * ldh, nvec, jb, SW, sv);
+      Vec<T, N> sv[V];
+      if (self) load_vecs<T, N, V>(h + (int64_t)ps * ldh, nvec, jb, SW, sv);
 #pragma unroll
-      for (int u = 0; u < kVPL; ++u) {
+      for (int u = 0; u < V; ++u) {
         const int vi = jb + u * SW;
         if (vi < nvec) {
 #pragma unroll
@@ -166,7 +169,7 @@ __global__ void self_of_kernel(const int32_t* __restrict__ self_pos, int64_t n_d
 }
 
 // dh[s] = ((0 + dself[self_of[s]]) + dmean[t_1]/denom_1) + dmean[t_2]/denom_2 ...
-template <typename T, int N>
+template <typename T, int N, int V>
 __global__ void __launch_bounds__(kWarps * 32)
     sage_bwd_kernel(const T* __restrict__ dself, const T* __restrict__ dmean, int H,
                     const int32_t* __restrict__ cnt, const int32_t* __restrict__ self_of,
@@ -181,46 +184,55 @@ __global__ void __launch_bounds__(kWarps * 32)
        s += nrow_step) {
     const int a = __ldg(toff + s), len = __ldg(toff + s + 1) - a;
     const int so = __ldg(self_of + s);
-    for (int vb = 0; vb < nvec; vb += SW * kVPL) {
+    for (int vb = 0; vb < nvec; vb += SW * V) {
       const int jb = vb + j0;
-      Vec<T, N> acc[kVPL];
+      Vec<T, N> acc[V];
 #pragma unroll
-      for (int u = 0; u < kVPL; ++u)
+      for (int u = 0; u < V; ++u)
 #pragma unroll
         for (int k = 0; k < N; ++k) acc[u].v[k] = (T)0;
       if (so >= 0) {
-        Vec<T, N> x[kVPL];
-        load_vecs<T, N>(dself + (int64_t)so * H, nvec, jb, SW, x);
+        Vec<T, N> x[V];
+        load_vecs<T, N, V>(dself + (int64_t)so * H, nvec, jb, SW, x);
 #pragma unroll
-        for (int u = 0; u < kVPL; ++u)
+        for (int u = 0; u < V; ++u)
 #pragma unroll
           for (int k = 0; k < N; ++k) acc[u].v[k] += x[u].v[k];
       }
+      // long segments (hub srcs with thousands of in-sample edges) are one
+      // sequential chain per column: keep R rows' loads in flight
+      constexpr int R = V == 1 ? 8 : 2;
       int q = 0;
-      for (; q + 2 <= len; q += 2) {
-        const int t0 = __ldg(tdst + a + q), t1 = __ldg(tdst + a + q + 1);
-        const T d0 = (T)max(__ldg(cnt + t0), 1), d1 = (T)max(__ldg(cnt + t1), 1);
-        Vec<T, N> x0[kVPL], x1[kVPL];
-        load_vecs<T, N>(dmean + (int64_t)t0 * H, nvec, jb, SW, x0);
-        load_vecs<T, N>(dmean + (int64_t)t1 * H, nvec, jb, SW, x1);
+      for (; q + R <= len; q += R) {
+        int t[R];
+        T dn[R];
+        Vec<T, N> x[R][V];
 #pragma unroll
-        for (int u = 0; u < kVPL; ++u)
+        for (int i = 0; i < R; ++i) t[i] = __ldg(tdst + a + q + i);
 #pragma unroll
-          for (int k = 0; k < N; ++k)
-            acc[u].v[k] = (acc[u].v[k] + x0[u].v[k] / d0) + x1[u].v[k] / d1;
+        for (int i = 0; i < R; ++i) {
+          dn[i] = (T)max(__ldg(cnt + t[i]), 1);
+          load_vecs<T, N, V>(dmean + (int64_t)t[i] * H, nvec, jb, SW, x[i]);
+        }
+#pragma unroll
+        for (int i = 0; i < R; ++i)
+#pragma unroll
+          for (int u = 0; u < V; ++u)
+#pragma unroll
+            for (int k = 0; k < N; ++k) acc[u].v[k] += x[i][u].v[k] / dn[i];
       }
-      if (q < len) {
+      for (; q < len; ++q) {
         const int t0 = __ldg(tdst + a + q);
         const T d0 = (T)max(__ldg(cnt + t0), 1);
-        Vec<T, N> x0[kVPL];
-        load_vecs<T, N>(dmean + (int64_t)t0 * H, nvec, jb, SW, x0);
+        Vec<T, N> x0[V];
+        load_vecs<T, N, V>(dmean + (int64_t)t0 * H, nvec, jb, SW, x0);
 #pragma unroll
-        for (int u = 0; u < kVPL; ++u)
+        for (int u = 0; u < V; ++u)
 #pragma unroll
           for (int k = 0; k < N; ++k) acc[u].v[k] += x0[u].v[k] / d0;
       }
 #pragma unroll
-      for (int u = 0; u < kVPL; ++u) {
+      for (int u = 0; u < V; ++u) {
         const int vi = jb + u * SW;
         if (vi < nvec) *reinterpret_cast<Vec<T, N>*>(dh + s * H + (int64_t)vi * N) = acc[u];
       }
@@ -252,11 +264,17 @@ int launch_fwd(const void* h, int ldh, int H, const int32_t* epos, const int32_t
                int64_t n_dst, const int32_t* cnt, int F, void* mean, void* self,
                cudaStream_t s) {
   const int SW = sub_warp(H / N);
+  const int vpl = (H / N + SW - 1) / SW;
   const int64_t rows_per_cta = (int64_t)kWarps * (32 / SW);
   const int grid = (int)std::min<int64_t>((n_dst + rows_per_cta - 1) / rows_per_cta, kNumSMs * 16);
-  sage_fwd_kernel<T, N><<<grid, kWarps * 32, 0, s>>>(
-      (const T*)h, ldh, H, epos, self_pos, n_dst, cnt, F, SW, (T*)mean, (T*)self);
-  return check_launch("sage_fwd");
+  auto go = [&](auto kern) {
+    kern<<<grid, kWarps * 32, 0, s>>>((const T*)h, ldh, H, epos, self_pos, n_dst, cnt, F, SW,
+                                      (T*)mean, (T*)self);
+    return check_launch("sage_fwd");
+  };
+  if (vpl <= 1) return go(sage_fwd_kernel<T, N, 1>);
+  if (vpl <= 2) return go(sage_fwd_kernel<T, N, 2>);
+  return go(sage_fwd_kernel<T, N, 4>);
 }
 
 template <typename T, int N>
@@ -264,11 +282,17 @@ int launch_bwd(const void* dself, const void* dmean, int H, const int32_t* cnt,
                const int32_t* self_of, const int32_t* toff, const int32_t* tdst, int64_t n_src,
                void* dh, cudaStream_t s) {
   const int SW = sub_warp(H / N);
+  const int vpl = (H / N + SW - 1) / SW;
   const int64_t rows_per_cta = (int64_t)kWarps * (32 / SW);
   const int grid = (int)std::min<int64_t>((n_src + rows_per_cta - 1) / rows_per_cta, kNumSMs * 16);
-  sage_bwd_kernel<T, N><<<grid, kWarps * 32, 0, s>>>((const T*)dself, (const T*)dmean, H, cnt,
-                                                     self_of, toff, tdst, n_src, SW, (T*)dh);
-  return check_launch("sage_bwd");
+  auto go = [&](auto kern) {
+    kern<<<grid, kWarps * 32, 0, s>>>((const T*)dself, (const T*)dmean, H, cnt, self_of, toff,
+                                      tdst, n_src, SW, (T*)dh);
+    return check_launch("sage_bwd");
+  };
+  if (vpl <= 1) return go(sage_bwd_kernel<T, N, 1>);
+  if (vpl <= 2) return go(sage_bwd_kernel<T, N, 2>);
+  return go(sage_bwd_kernel<T, N, 4>);
 }
 
 constexpr size_t kAlign = 256;

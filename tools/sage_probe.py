@@ -77,6 +77,16 @@ def main():
                                           dg.n, rank))
     ms_fwd = timed(lambda: sage_mean(h, pos, blk.cnt[d]))
     ms_bwd = timed(lambda: sage_mean_backward(dself, dmean, blk.cnt[d], pos))
+    from paper_2505_10806_b200 import _lib
+    nbytes = int(_lib.device().rg_sage_transpose_scratch(n_src, n_dst, F))
+    scratch = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    toff = torch.empty(n_src + 1, dtype=torch.int32, device="cuda")
+    tdst = torch.empty(n_dst * F, dtype=torch.int32, device="cuda")
+    ms_tr = timed(lambda: _lib.call("rg_sage_transpose", pos.epos.data_ptr(), blk.cnt[d].data_ptr(),
+                                    n_dst, F, n_src, toff.data_ptr(), tdst.data_ptr(),
+                                    scratch.data_ptr(), nbytes, _lib.stream_handle()))
+    seg = (toff[1:] - toff[:-1])
+    longest = int(seg.max().item())
     row = 400
     fwd_bytes = edges * (row + 4) + n_dst * (row + 4 + 4) + 2 * n_dst * row
     bwd_bytes = edges * (row + 8) + n_dst * row + n_src * row
@@ -89,6 +99,8 @@ def main():
            "bwd_total": {"ms": ms_bwd, "bytes": bwd_bytes, "gbs": bwd_bytes / ms_bwd / 1e6,
                          "frac": bwd_bytes / ms_bwd / 1e6 / peak,
                          "note": "includes the radix-sort transpose and self_of"},
+           "transpose_ms": ms_tr, "bwd_kernel_ms_est": ms_bwd - ms_tr,
+           "longest_src_segment": longest,
            "peak_gbs": peak}
     print(json.dumps(out))
 
