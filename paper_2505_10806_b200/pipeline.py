@@ -374,7 +374,13 @@ class WorkerPipeline:
                 bases[q] = t.data_ptr()
             peer_mask = 0  # every row is local now
         cnt = ptr(self.counters) + i0 * _lib.RG_NCOUNTERS * 4
-        if self.gather_mode == "window" and ng <= 128 and peer_mask == 0:
+        # the bitmap-driven (staged union) gather pays off when the group's
+        # batches share rows: G * cap_in / n bounds the mean reuse of a union
+        # row (Products G = 128: 56, measured ~35 -> 5.97 vs 6.70 ms); for
+        # sparse groups (papers100M-shaped, G = 8: 0.31) the id-list queue
+        # gather is faster (15.8 vs ~3.5 ms per launch)
+        dense = ng * self.cap_in >= 4 * self.dg.n
+        if self.gather_mode == "window" and dense and ng <= 128 and peer_mask == 0:
             # id-window-major, straight from the group's input bitmaps
             _lib.call("rg_gather_window", ptr(smp.bm), ptr(smp.wpre), self.dg.nwords, ng,
                       self.cap_in, ptr(route), bases_array(bases), st.src_stride, st.stride,
