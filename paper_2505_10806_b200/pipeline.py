@@ -68,6 +68,14 @@ class WorkerPipeline:
         self.rows = self.row_bufs[0]
         self.s_sample = torch.cuda.Stream()
         self.s_gather = torch.cuda.Stream()
+        # the group prefetch (N > 1) gets its own stream: sample(k+1) no longer
+        # queues behind prefetch(k) (papers100M-shaped N = 2: 1,536 vs 1,425
+        # batches/s; Products unchanged).  Stream priorities and a deferred
+        # schedule (sample k + gather k-1 on one stream, the copy beside them)
+        # measured no better: co-running kernels slow each other
+        self.s_prefetch = torch.cuda.Stream()
+        self.prefetch_stream = os.environ.get("RG_PREFETCH_STREAM", "1") != "0"
+        self.ev_prefetched = [torch.cuda.Event() for _ in range(self.nbuf)]
         self.ev_sampled = [torch.cuda.Event() for _ in range(self.nbuf)]
         self.ev_gathered = [torch.cuda.Event() for _ in range(self.nbuf)]
         self.k = 0
@@ -320,12 +328,21 @@ class WorkerPipeline:
                 smp.rng.copy_(host_seeds[2], non_blocking=True)
             smp.run(ng)
             e1 = mark("sample", self.s_sample, e0)
-            if self.prefetch:
+            if self.prefetch and not self.prefetch_stream:
                 self.prefetch_group(ng, smp, slot)
                 mark("prefetch", self.s_sample, e1)
             self.ev_sampled[slot].record(self.s_sample)
+        gate = self.ev_sampled[slot]
+        if self.prefetch and self.prefetch_stream:
+            with torch.cuda.stream(self.s_prefetch):
+                self.s_prefetch.wait_event(self.ev_sampled[slot])
+                e3 = mark("prefetch", self.s_prefetch)
+                self.prefetch_group(ng, smp, slot)
+                mark("prefetch", self.s_prefetch, e3)
+                self.ev_prefetched[slot].record(self.s_prefetch)
+            gate = self.ev_prefetched[slot]
         with torch.cuda.stream(self.s_gather):
-            self.s_gather.wait_event(self.ev_sampled[slot])
+            self.s_gather.wait_event(gate)
             e2 = mark("gather", self.s_gather)
             self.gather(ng, i0, smp, self.row_bufs[slot], slot=slot, prefetched=True)
             mark("gather", self.s_gather, e2)
@@ -346,11 +363,13 @@ class WorkerPipeline:
         """Order both side streams after the current stream's work."""
         cur = torch.cuda.current_stream()
         self.s_sample.wait_stream(cur)
+        self.s_prefetch.wait_stream(cur)
         self.s_gather.wait_stream(cur)
 
     def sync_streams(self) -> None:
         cur = torch.cuda.current_stream()
         cur.wait_stream(self.s_sample)
+        cur.wait_stream(self.s_prefetch)
         cur.wait_stream(self.s_gather)
 
     def gather(self, ng: int, i0: int, smp=None, rows=None, slot: int = 0,
