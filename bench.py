@@ -664,7 +664,13 @@ def main():
                 "overlapped": run_train_leg(dg, store, part, train, cfg, hot, g.labels, 32,
                                             args.train_groups, True),
                 "serial": run_train_leg(dg, store, part, train, cfg, hot, g.labels, 32,
-                                        args.train_groups, False)}
+                                        args.train_groups, False),
+                "overlapped_eager": run_train_leg(dg, store, part, train, cfg, hot, g.labels, 32,
+                                                  args.train_groups, True, graphs=False),
+                "note": "sample+gather+GraphSAGE step (bit-exact aggregation, fp32 cuBLAS "
+                        "GEMMs, SGD) per batch; overlapped = GroupProducer thread samples / "
+                        "gathers group k+1 on side streams while group k trains; cuda_graphs "
+                        "= each (slot, batch) step replayed from a captured graph"}
     if rank == 0 and world == 1 and not args.no_cpu and not cfg.get("device_features"):
         result = cpu_baseline(cpu_state(g, book.owner, cfg, hot_np, part), args.cpu_seconds, nb)
 
@@ -691,7 +697,7 @@ def main():
                "inputs larger than L2 (feature shards %.0f MB; bundle %.0f MB/batch)")
               % ((feat_bytes / 1e6,) if flush
                  else (feat_bytes / 1e6, float(rows_b.mean()) * d * 4 / 1e6)),
-        "roofline": {"kernel": "gather_queue_kernel (rg_gather_bundle)", "bound": "hbm",
+        "roofline": {"kernel": getattr(pipe, "gather_kernel", "rg_gather_bundle"), "bound": "hbm",
                      "achieved": achieved, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic_b,
                      "bytes_per_launch": launch_bytes / args.steps,
@@ -873,7 +879,7 @@ def run_group_leg(dg, store, part, train, cfg, hot, group: int, nbuf: int, steps
 
 
 def run_train_leg(dg, store, part, train, cfg, hot, labels_np, group: int, groups: int,
-                  overlap: bool):
+                  overlap: bool, graphs: bool = True):
     """Consumer attached: every batch sampled + gathered AND trained (the
     device GraphSAGE step of train.py: bit-exact aggregation, cuBLAS fp32
     GEMMs, SGD), `groups` groups of `group` batches.  overlap=True: the
@@ -895,9 +901,14 @@ def run_train_leg(dg, store, part, train, cfg, hot, labels_np, group: int, group
     labels = torch.from_numpy(np.asarray(labels_np)).cuda()
     params = model.init_params(d, 32, cfg["classes"], len(cfg["fanouts"]), 1234)
     loss_sum = torch.zeros((), dtype=torch.float64, device="cuda")
+    trainer = model.GraphTrainer(params, labels, d, dg.n, 0.05) if graphs else None
 
     def train_group(smp, rows_buf, ng, nf):
         nonlocal params
+        if trainer is not None:
+            for b in range(ng):
+                trainer.step(smp, rows_buf, b)
+            return
         for b in range(ng):
             blk = model.block_from_slot(smp, b, nf[:, b])
             rows = rows_buf[b, : int(nf[smp.L, b]), :d]
@@ -920,18 +931,26 @@ def run_train_leg(dg, store, part, train, cfg, hot, labels_np, group: int, group
                 ng = pipe.step(i0)
                 train_group(pipe.sampler, pipe.rows, ng, pipe.sampler.nfront[:, :ng].cpu().numpy())
 
+    n_full = max(1, pipe.nb // pipe.G)
+    group = pipe.G
     epoch_part([0])  # warm-up: allocator, cuBLAS handles
+    if graphs:  # capture every (slot, batch) graph outside the timing
+        epoch_part([group % (n_full * group)] if n_full > 1 else [0])
+        if trainer is not None and len(trainer.graphs) < 2 * group:
+            epoch_part([0])
     torch.cuda.synchronize()
     t = time.perf_counter()
-    starts = [(1 + k) * group for k in range(groups)]
+    starts = [((1 + k) % n_full) * group for k in range(groups)]
     epoch_part(starts)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t
-    loss = float(loss_sum.item())
-    del pipe
+    loss = float((trainer.loss_sum if trainer is not None else loss_sum).item())
+    captures = trainer.captures if trainer is not None else 0
+    del pipe, trainer
     torch.cuda.empty_cache()
     return {"value": groups * group / wall, "unit": "batches/s", "batches": groups * group,
-            "group": group, "overlap": overlap, "loss_sum": loss}
+            "group": group, "overlap": overlap, "cuda_graphs": graphs, "graph_captures": captures,
+            "loss_sum": loss}
 
 
 def run_e2e_host_rows(pipe, cfg, args, world):

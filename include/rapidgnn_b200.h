@@ -228,19 +228,25 @@ int rg_scatter_rows(const int32_t* d_ids, int64_t n, const uint32_t* d_route,
  * (rank[src_front[j]] = j), d_epos[t*fanout + r] = position of the r-th
  * sampled neighbour of dst row t (-1 for r >= cnt[t]), d_self_pos[t] =
  * position of dst_front[t].  Frontiers are nested (dst ⊂ src) and every
- * ELL entry is a member of src_front (the sampler's contract).          */
+ * ELL entry is a member of src_front (the sampler's contract).
+ * Device counts: every aggregation entry point takes optional device words
+ * d_n_src / d_n_dst (e.g. a sampler slot's nfront entries).  When given, the
+ * host n_src / n_dst are capacities, the live counts are read on the device
+ * (no host sync: the whole training step can be captured in a CUDA graph)
+ * and rows past them are padding (no edges, zero outputs).  NULL: the host
+ * sizes are the counts.                                                  */
 int rg_sage_positions(const int32_t* d_src_front, int64_t n_src, const int32_t* d_dst_front,
                       int64_t n_dst, const int32_t* d_ell, const int32_t* d_cnt, int32_t fanout,
-                      int64_t n_nodes, int32_t* d_rank, int32_t* d_epos, int32_t* d_self_pos,
-                      void* stream);
+                      int64_t n_nodes, const int32_t* d_n_src, const int32_t* d_n_dst,
+                      int32_t* d_rank, int32_t* d_epos, int32_t* d_self_pos, void* stream);
 /* mean[t] = (in stored order, sum of h[epos[t, r]]) / max(cnt_t, 1) and
  * self[t] = h[self_pos[t]] (self may be NULL); h rows ldh elements apart,
  * outputs dense [n_dst, H].  dtype RG_DTYPE_F32 / F64; in-order, IEEE
  * divide: bit-exact with the reference's np.add.at / divide.            */
 int rg_sage_mean_fwd(int32_t dtype, const void* d_h, int32_t H, int32_t ldh,
                      const int32_t* d_epos, const int32_t* d_self_pos, int64_t n_dst,
-                     const int32_t* d_cnt, int32_t fanout, void* d_mean, void* d_self,
-                     void* stream);
+                     const int32_t* d_n_dst, const int32_t* d_cnt, int32_t fanout, void* d_mean,
+                     void* d_self, void* stream);
 /* Transposed edge index for the backward: edges grouped by src position,
  * ascending dst row inside a group (the reference's edge order for that
  * src), any group length.  d_toff n_src+1, d_tdst n_dst*fanout; scratch
@@ -256,7 +262,8 @@ int rg_sage_transpose(const int32_t* d_epos, const int32_t* d_cnt, int64_t n_dst
 int rg_sage_mean_bwd(int32_t dtype, const void* d_dself, const void* d_dmean, int64_t n_dst,
                      int32_t H, const int32_t* d_cnt, const int32_t* d_self_pos,
                      const int32_t* d_toff, const int32_t* d_tdst, int64_t n_src,
-                     int32_t* d_self_of, void* d_dh, void* stream);
+                     const int32_t* d_n_src, const int32_t* d_n_dst, int32_t* d_self_of,
+                     void* d_dh, void* stream);
 
 /* ---- host-side graph materialisation (graph.py, partition.py) ------- */
 int rg_philox_raw(uint64_t key0, uint64_t key1, int64_t count, uint64_t* h_out);

@@ -66,14 +66,14 @@ _SIGNATURES = {
     "rg_group_union": (c_int32, [P, c_int64, c_int32, P, P, P]),
     "rg_prefetch_rows": (c_int32, [P, P, c_int64, P, P, P, c_int32, c_int32, P]),
     "rg_scatter_rows": (c_int32, [P, c_int64, P, P, c_int32, P, c_int32, c_int32, P]),
-    "rg_sage_positions": (c_int32, [P, c_int64, P, c_int64, P, P, c_int32, c_int64, P, P, P,
-                                    P]),
-    "rg_sage_mean_fwd": (c_int32, [c_int32, P, c_int32, c_int32, P, P, c_int64, P, c_int32, P,
-                                   P, P]),
+    "rg_sage_positions": (c_int32, [P, c_int64, P, c_int64, P, P, c_int32, c_int64, P, P, P, P,
+                                    P, P]),
+    "rg_sage_mean_fwd": (c_int32, [c_int32, P, c_int32, c_int32, P, P, c_int64, P, P, c_int32,
+                                   P, P, P]),
     "rg_sage_transpose_scratch": (c_int64, [c_int64, c_int64, c_int32]),
     "rg_sage_transpose": (c_int32, [P, P, c_int64, c_int32, c_int64, P, P, P, c_int64, P]),
     "rg_sage_mean_bwd": (c_int32, [c_int32, P, P, c_int64, c_int32, P, P, P, P, c_int64, P, P,
-                                   P]),
+                                   P, P, P]),
     "rg_prng_raw": (c_int32, [c_int32, c_uint64, c_uint64, c_int64, P]),
     "rg_prng_select": (c_int32, [c_int32, c_uint64, c_uint64, c_int32, c_int32, P]),
     "rg_philox_raw": (c_int32, [c_uint64, c_uint64, c_int64, P]),

@@ -44,12 +44,18 @@ def edges_to_ell(dst_front: np.ndarray, src: np.ndarray, dst: np.ndarray):
 @dataclass
 class LevelPositions:
     """One level's resolved positions: epos [n_dst*F] (src position of every
-    ELL edge, -1 past a row's count), self_pos [n_dst]."""
+    ELL edge, -1 past a row's count), self_pos [n_dst].  With device counts
+    (d_n_src / d_n_dst: addresses of int32 words, e.g. a sampler slot's
+    nfront entries) n_src / n_dst are capacities and rows past the live
+    counts are zero padding — nothing here then syncs with the host, so a
+    whole training step can be captured in a CUDA graph."""
 
     epos: torch.Tensor
     self_pos: torch.Tensor
     n_src: int
     fanout: int
+    d_n_src: int | None = None
+    d_n_dst: int | None = None
 
 
 def _dtype_code(t: torch.Tensor) -> int:
@@ -60,9 +66,12 @@ def _dtype_code(t: torch.Tensor) -> int:
 
 def sage_positions(src_front: torch.Tensor, dst_front: torch.Tensor, ell: torch.Tensor,
                    cnt: torch.Tensor, fanout: int, n_nodes: int,
-                   rank: torch.Tensor | None = None) -> LevelPositions:
+                   rank: torch.Tensor | None = None, d_n_src: int | None = None,
+                   d_n_dst: int | None = None) -> LevelPositions:
     """Ranks of every sampled edge's src and of every dst in src_front
-    (rank: optional int32 [n_nodes] scratch, reusable across levels)."""
+    (rank: optional int32 [n_nodes] scratch, reusable across levels).
+    d_n_src / d_n_dst: optional device counts (the tensors are then
+    capacity-sized)."""
     n_src, n_dst = int(src_front.numel()), int(dst_front.numel())
     dev = src_front.device
     if rank is None:
@@ -70,9 +79,9 @@ def sage_positions(src_front: torch.Tensor, dst_front: torch.Tensor, ell: torch.
     epos = torch.empty(max(1, n_dst * fanout), dtype=I32, device=dev)
     self_pos = torch.empty(max(n_dst, 1), dtype=I32, device=dev)
     _lib.call("rg_sage_positions", ptr(src_front), n_src, ptr(dst_front), n_dst, ptr(ell),
-              ptr(cnt), fanout, n_nodes, ptr(rank), ptr(epos), ptr(self_pos),
+              ptr(cnt), fanout, n_nodes, d_n_src, d_n_dst, ptr(rank), ptr(epos), ptr(self_pos),
               _lib.stream_handle())
-    return LevelPositions(epos, self_pos[:n_dst], n_src, fanout)
+    return LevelPositions(epos, self_pos[:n_dst], n_src, fanout, d_n_src, d_n_dst)
 
 
 def sage_mean(h: torch.Tensor, pos: LevelPositions, cnt: torch.Tensor, H: int | None = None):
@@ -90,7 +99,8 @@ def sage_mean(h: torch.Tensor, pos: LevelPositions, cnt: torch.Tensor, H: int | 
     mean = torch.empty((max(n_dst, 1), H), dtype=h.dtype, device=dev)
     hself = torch.empty((max(n_dst, 1), H), dtype=h.dtype, device=dev)
     _lib.call("rg_sage_mean_fwd", code, ptr(h), H, h.stride(0), ptr(pos.epos), ptr(pos.self_pos),
-              n_dst, ptr(cnt), pos.fanout, ptr(mean), ptr(hself), _lib.stream_handle())
+              n_dst, pos.d_n_dst, ptr(cnt), pos.fanout, ptr(mean), ptr(hself),
+              _lib.stream_handle())
     return mean[:n_dst], hself[:n_dst]
 
 
@@ -117,5 +127,6 @@ def sage_mean_backward(dself: torch.Tensor, dmean: torch.Tensor, cnt: torch.Tens
     self_of = torch.empty(n_src, dtype=I32, device=dev)
     dh = torch.empty((n_src, H), dtype=dmean.dtype, device=dev)
     _lib.call("rg_sage_mean_bwd", code, ptr(dself), ptr(dmean), n_dst, H, ptr(cnt),
-              ptr(pos.self_pos), ptr(toff), ptr(tdst), n_src, ptr(self_of), ptr(dh), s)
+              ptr(pos.self_pos), ptr(toff), ptr(tdst), n_src, pos.d_n_src, pos.d_n_dst,
+              ptr(self_of), ptr(dh), s)
     return dh

@@ -28,9 +28,17 @@ namespace {
 
 constexpr int kWarps = 8;
 
+// live count: the device word when given (a sampler slot's nfront entry, so
+// the call needs no host sync and can be captured in a CUDA graph; the host
+// size is then the capacity), else the host size itself
+__device__ __forceinline__ int64_t live_count(const int32_t* d_n, int64_t cap) {
+  return d_n ? min((int64_t)__ldg(d_n), cap) : cap;
+}
+
 // ---------------------------------------------------------------- positions
-__global__ void rank_scatter_kernel(const int32_t* __restrict__ front, int64_t n,
-                                    int32_t* __restrict__ rank) {
+__global__ void rank_scatter_kernel(const int32_t* __restrict__ front, int64_t cap,
+                                    const int32_t* __restrict__ d_n, int32_t* __restrict__ rank) {
+  const int64_t n = live_count(d_n, cap);
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
        j += (int64_t)gridDim.x * blockDim.x)
     rank[front[j]] = (int32_t)j;
@@ -38,18 +46,22 @@ __global__ void rank_scatter_kernel(const int32_t* __restrict__ front, int64_t n
 
 // epos[t*F + r] = rank of ell[t*F + r] (r < cnt[t]), -1 past the row's count;
 // self_pos[t] = rank of dst_front[t] (frontiers are nested: dst ⊂ src)
+// rows past the live count (capacity padding) get no edges and self row 0
 __global__ void edge_pos_kernel(const int32_t* __restrict__ rank,
-                                const int32_t* __restrict__ dst_front, int64_t n_dst,
+                                const int32_t* __restrict__ dst_front, int64_t cap_dst,
+                                const int32_t* __restrict__ d_ndst,
                                 const int32_t* __restrict__ ell, const int32_t* __restrict__ cnt,
                                 int F, int32_t* __restrict__ epos,
                                 int32_t* __restrict__ self_pos) {
-  const int64_t total = n_dst * F;
+  const int64_t n_dst = live_count(d_ndst, cap_dst);
+  const int64_t total = cap_dst * F;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = i / F;
     const int r = (int)(i - t * F);
-    epos[i] = r < __ldg(cnt + t) ? __ldg(rank + __ldg(ell + i)) : -1;
-    if (r == 0) self_pos[t] = __ldg(rank + __ldg(dst_front + t));
+    const bool live = t < n_dst;
+    epos[i] = live && r < __ldg(cnt + t) ? __ldg(rank + __ldg(ell + i)) : -1;
+    if (r == 0) self_pos[t] = live ? __ldg(rank + __ldg(dst_front + t)) : 0;
   }
 }
 
@@ -77,17 +89,19 @@ __device__ __forceinline__ void load_vecs(const T* __restrict__ row, int nvec, i
 template <typename T, int N, int V>
 __global__ void __launch_bounds__(kWarps * 32)
     sage_fwd_kernel(const T* __restrict__ h, int ldh, int H, const int32_t* __restrict__ epos,
-                    const int32_t* __restrict__ self_pos, int64_t n_dst,
-                    const int32_t* __restrict__ cnt, int F, int SW, T* __restrict__ mean,
-                    T* __restrict__ self) {
+                    const int32_t* __restrict__ self_pos, int64_t cap_dst,
+                    const int32_t* __restrict__ d_ndst, const int32_t* __restrict__ cnt, int F,
+                    int SW, T* __restrict__ mean, T* __restrict__ self) {
+  const int64_t n_live = live_count(d_ndst, cap_dst);
   const int lane = lane_id();
   const int rpw = 32 / SW;  // rows per warp
   const int grp = lane / SW, j0 = lane % SW;
   const int nvec = H / N;
   const int64_t nrow_step = (int64_t)gridDim.x * kWarps * rpw;
-  for (int64_t t = ((int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5)) * rpw + grp; t < n_dst;
+  for (int64_t t = ((int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5)) * rpw + grp; t < cap_dst;
        t += nrow_step) {
-    const int c = __ldg(cnt + t);
+    const bool live = t < n_live;  // padding rows: mean = self = 0
+    const int c = live ? __ldg(cnt + t) : 0;
     const T denom = (T)max(c, 1);
     const int32_t* ep = epos + t * F;
     const int ps = __ldg(self_pos + t);
@@ -121,7 +135,11 @@ __global__ void __launch_bounds__(kWarps * 32)
           for (int k = 0; k < N; ++k) acc[u].v[k] += x0[u].v[k];
       }
       Vec<T, N> sv[V];
-      if (self) load_vecs<T, N, V>(h + (int64_t)ps * ldh, nvec, jb, SW, sv);
+#pragma unroll
+      for (int u = 0; u < V; ++u)
+#pragma unroll
+        for (int k = 0; k < N; ++k) sv[u].v[k] = (T)0;
+      if (self && live) load_vecs<T, N, V>(h + (int64_t)ps * ldh, nvec, jb, SW, sv);
 #pragma unroll
       for (int u = 0; u < V; ++u) {
         const int vi = jb + u * SW;
@@ -161,8 +179,10 @@ __global__ void transpose_keys_kernel(const int32_t* __restrict__ epos, int64_t 
   }
 }
 
-__global__ void self_of_kernel(const int32_t* __restrict__ self_pos, int64_t n_dst,
+__global__ void self_of_kernel(const int32_t* __restrict__ self_pos, int64_t cap_dst,
+                               const int32_t* __restrict__ d_ndst,
                                int32_t* __restrict__ self_of) {
+  const int64_t n_dst = live_count(d_ndst, cap_dst);
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_dst;
        t += (int64_t)gridDim.x * blockDim.x)
     self_of[self_pos[t]] = (int32_t)t;
@@ -174,16 +194,19 @@ __global__ void __launch_bounds__(kWarps * 32)
     sage_bwd_kernel(const T* __restrict__ dself, const T* __restrict__ dmean, int H,
                     const int32_t* __restrict__ cnt, const int32_t* __restrict__ self_of,
                     const int32_t* __restrict__ toff, const int32_t* __restrict__ tdst,
-                    int64_t n_src, int SW, T* __restrict__ dh) {
+                    int64_t cap_src, const int32_t* __restrict__ d_nsrc, int SW,
+                    T* __restrict__ dh) {
+  const int64_t n_live = live_count(d_nsrc, cap_src);
   const int lane = lane_id();
   const int rpw = 32 / SW;
   const int grp = lane / SW, j0 = lane % SW;
   const int nvec = H / N;
   const int64_t nrow_step = (int64_t)gridDim.x * kWarps * rpw;
-  for (int64_t s = ((int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5)) * rpw + grp; s < n_src;
+  for (int64_t s = ((int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5)) * rpw + grp; s < cap_src;
        s += nrow_step) {
-    const int a = __ldg(toff + s), len = __ldg(toff + s + 1) - a;
-    const int so = __ldg(self_of + s);
+    const bool live = s < n_live;  // padding rows: dh = 0
+    const int a = live ? __ldg(toff + s) : 0, len = live ? __ldg(toff + s + 1) - a : 0;
+    const int so = live ? __ldg(self_of + s) : -1;
     for (int vb = 0; vb < nvec; vb += SW * V) {
       const int jb = vb + j0;
       Vec<T, N> acc[V];
@@ -261,15 +284,15 @@ int sub_warp(int nvec) {
 
 template <typename T, int N>
 int launch_fwd(const void* h, int ldh, int H, const int32_t* epos, const int32_t* self_pos,
-               int64_t n_dst, const int32_t* cnt, int F, void* mean, void* self,
-               cudaStream_t s) {
+               int64_t n_dst, const int32_t* d_ndst, const int32_t* cnt, int F, void* mean,
+               void* self, cudaStream_t s) {
   const int SW = sub_warp(H / N);
   const int vpl = (H / N + SW - 1) / SW;
   const int64_t rows_per_cta = (int64_t)kWarps * (32 / SW);
   const int grid = (int)std::min<int64_t>((n_dst + rows_per_cta - 1) / rows_per_cta, kNumSMs * 16);
   auto go = [&](auto kern) {
-    kern<<<grid, kWarps * 32, 0, s>>>((const T*)h, ldh, H, epos, self_pos, n_dst, cnt, F, SW,
-                                      (T*)mean, (T*)self);
+    kern<<<grid, kWarps * 32, 0, s>>>((const T*)h, ldh, H, epos, self_pos, n_dst, d_ndst, cnt, F,
+                                      SW, (T*)mean, (T*)self);
     return check_launch("sage_fwd");
   };
   if (vpl <= 1) return go(sage_fwd_kernel<T, N, 1>);
@@ -280,14 +303,14 @@ int launch_fwd(const void* h, int ldh, int H, const int32_t* epos, const int32_t
 template <typename T, int N>
 int launch_bwd(const void* dself, const void* dmean, int H, const int32_t* cnt,
                const int32_t* self_of, const int32_t* toff, const int32_t* tdst, int64_t n_src,
-               void* dh, cudaStream_t s) {
+               const int32_t* d_nsrc, void* dh, cudaStream_t s) {
   const int SW = sub_warp(H / N);
   const int vpl = (H / N + SW - 1) / SW;
   const int64_t rows_per_cta = (int64_t)kWarps * (32 / SW);
   const int grid = (int)std::min<int64_t>((n_src + rows_per_cta - 1) / rows_per_cta, kNumSMs * 16);
   auto go = [&](auto kern) {
     kern<<<grid, kWarps * 32, 0, s>>>((const T*)dself, (const T*)dmean, H, cnt, self_of, toff,
-                                      tdst, n_src, SW, (T*)dh);
+                                      tdst, n_src, d_nsrc, SW, (T*)dh);
     return check_launch("sage_bwd");
   };
   if (vpl <= 1) return go(sage_bwd_kernel<T, N, 1>);
@@ -320,41 +343,41 @@ using namespace rg;
 extern "C" int rg_sage_positions(const int32_t* d_src_front, int64_t n_src,
                                  const int32_t* d_dst_front, int64_t n_dst, const int32_t* d_ell,
                                  const int32_t* d_cnt, int32_t fanout, int64_t n_nodes,
-                                 int32_t* d_rank, int32_t* d_epos, int32_t* d_self_pos,
-                                 void* stream) {
+                                 const int32_t* d_n_src, const int32_t* d_n_dst, int32_t* d_rank,
+                                 int32_t* d_epos, int32_t* d_self_pos, void* stream) {
   RG_REQUIRE(n_src >= 1 && n_src <= INT32_MAX && n_dst >= 0 && fanout >= 1 && n_nodes >= n_src,
              "rg_sage_positions: bad sizes");
   RG_REQUIRE(n_dst * (int64_t)fanout < INT32_MAX, "rg_sage_positions: n_dst * fanout overflows");
   if (n_dst == 0) return RG_OK;
   cudaStream_t s = (cudaStream_t)stream;
   rank_scatter_kernel<<<(unsigned)std::min<int64_t>((n_src + 255) / 256, kNumSMs * 8), 256, 0, s>>>(
-      d_src_front, n_src, d_rank);
+      d_src_front, n_src, d_n_src, d_rank);
   int rc = check_launch("rank_scatter");
   if (rc) return rc;
   const int64_t total = n_dst * fanout;
   edge_pos_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, kNumSMs * 8), 256, 0, s>>>(
-      d_rank, d_dst_front, n_dst, d_ell, d_cnt, fanout, d_epos, d_self_pos);
+      d_rank, d_dst_front, n_dst, d_n_dst, d_ell, d_cnt, fanout, d_epos, d_self_pos);
   return check_launch("edge_pos");
 }
 
 extern "C" int rg_sage_mean_fwd(int32_t dtype, const void* d_h, int32_t H, int32_t ldh,
                                 const int32_t* d_epos, const int32_t* d_self_pos, int64_t n_dst,
-                                const int32_t* d_cnt, int32_t fanout, void* d_mean, void* d_self,
-                                void* stream) {
+                                const int32_t* d_n_dst, const int32_t* d_cnt, int32_t fanout,
+                                void* d_mean, void* d_self, void* stream) {
   RG_REQUIRE(H >= 1 && ldh >= H && n_dst >= 0 && fanout >= 1, "rg_sage_mean_fwd: bad sizes");
   RG_REQUIRE(dtype == RG_DTYPE_F32 || dtype == RG_DTYPE_F64, "rg_sage_mean_fwd: bad dtype");
   if (n_dst == 0) return RG_OK;
   cudaStream_t s = (cudaStream_t)stream;
   if (dtype == RG_DTYPE_F32) {
     switch (vec_width<float>(H, ldh, {d_h, d_mean, d_self})) {
-      case 4: return launch_fwd<float, 4>(d_h, ldh, H, d_epos, d_self_pos, n_dst, d_cnt, fanout, d_mean, d_self, s);
-      case 2: return launch_fwd<float, 2>(d_h, ldh, H, d_epos, d_self_pos, n_dst, d_cnt, fanout, d_mean, d_self, s);
-      default: return launch_fwd<float, 1>(d_h, ldh, H, d_epos, d_self_pos, n_dst, d_cnt, fanout, d_mean, d_self, s);
+      case 4: return launch_fwd<float, 4>(d_h, ldh, H, d_epos, d_self_pos, n_dst, d_n_dst, d_cnt, fanout, d_mean, d_self, s);
+      case 2: return launch_fwd<float, 2>(d_h, ldh, H, d_epos, d_self_pos, n_dst, d_n_dst, d_cnt, fanout, d_mean, d_self, s);
+      default: return launch_fwd<float, 1>(d_h, ldh, H, d_epos, d_self_pos, n_dst, d_n_dst, d_cnt, fanout, d_mean, d_self, s);
     }
   }
   if (vec_width<double>(H, ldh, {d_h, d_mean, d_self}) == 2)
-    return launch_fwd<double, 2>(d_h, ldh, H, d_epos, d_self_pos, n_dst, d_cnt, fanout, d_mean, d_self, s);
-  return launch_fwd<double, 1>(d_h, ldh, H, d_epos, d_self_pos, n_dst, d_cnt, fanout, d_mean, d_self, s);
+    return launch_fwd<double, 2>(d_h, ldh, H, d_epos, d_self_pos, n_dst, d_n_dst, d_cnt, fanout, d_mean, d_self, s);
+  return launch_fwd<double, 1>(d_h, ldh, H, d_epos, d_self_pos, n_dst, d_n_dst, d_cnt, fanout, d_mean, d_self, s);
 }
 
 extern "C" int64_t rg_sage_transpose_scratch(int64_t n_src, int64_t n_dst, int32_t fanout) {
@@ -402,26 +425,27 @@ extern "C" int rg_sage_transpose(const int32_t* d_epos, const int32_t* d_cnt, in
 extern "C" int rg_sage_mean_bwd(int32_t dtype, const void* d_dself, const void* d_dmean,
                                 int64_t n_dst, int32_t H, const int32_t* d_cnt,
                                 const int32_t* d_self_pos, const int32_t* d_toff,
-                                const int32_t* d_tdst, int64_t n_src, int32_t* d_self_of,
-                                void* d_dh, void* stream) {
+                                const int32_t* d_tdst, int64_t n_src, const int32_t* d_n_src,
+                                const int32_t* d_n_dst, int32_t* d_self_of, void* d_dh,
+                                void* stream) {
   RG_REQUIRE(H >= 1 && n_src >= 1 && n_dst >= 0, "rg_sage_mean_bwd: bad sizes");
   RG_REQUIRE(dtype == RG_DTYPE_F32 || dtype == RG_DTYPE_F64, "rg_sage_mean_bwd: bad dtype");
   cudaStream_t s = (cudaStream_t)stream;
   if (cudaMemsetAsync(d_self_of, 0xff, sizeof(int32_t) * n_src, s) != cudaSuccess)
     return check_launch("bwd memset");
   if (n_dst > 0) {
-    self_of_kernel<<<kNumSMs * 2, 256, 0, s>>>(d_self_pos, n_dst, d_self_of);
+    self_of_kernel<<<kNumSMs * 2, 256, 0, s>>>(d_self_pos, n_dst, d_n_dst, d_self_of);
     int rc = check_launch("self_of");
     if (rc) return rc;
   }
   if (dtype == RG_DTYPE_F32) {
     switch (vec_width<float>(H, H, {d_dself, d_dmean, d_dh})) {
-      case 4: return launch_bwd<float, 4>(d_dself, d_dmean, H, d_cnt, d_self_of, d_toff, d_tdst, n_src, d_dh, s);
-      case 2: return launch_bwd<float, 2>(d_dself, d_dmean, H, d_cnt, d_self_of, d_toff, d_tdst, n_src, d_dh, s);
-      default: return launch_bwd<float, 1>(d_dself, d_dmean, H, d_cnt, d_self_of, d_toff, d_tdst, n_src, d_dh, s);
+      case 4: return launch_bwd<float, 4>(d_dself, d_dmean, H, d_cnt, d_self_of, d_toff, d_tdst, n_src, d_n_src, d_dh, s);
+      case 2: return launch_bwd<float, 2>(d_dself, d_dmean, H, d_cnt, d_self_of, d_toff, d_tdst, n_src, d_n_src, d_dh, s);
+      default: return launch_bwd<float, 1>(d_dself, d_dmean, H, d_cnt, d_self_of, d_toff, d_tdst, n_src, d_n_src, d_dh, s);
     }
   }
   if (vec_width<double>(H, H, {d_dself, d_dmean, d_dh}) == 2)
-    return launch_bwd<double, 2>(d_dself, d_dmean, H, d_cnt, d_self_of, d_toff, d_tdst, n_src, d_dh, s);
-  return launch_bwd<double, 1>(d_dself, d_dmean, H, d_cnt, d_self_of, d_toff, d_tdst, n_src, d_dh, s);
+    return launch_bwd<double, 2>(d_dself, d_dmean, H, d_cnt, d_self_of, d_toff, d_tdst, n_src, d_n_src, d_dh, s);
+  return launch_bwd<double, 1>(d_dself, d_dmean, H, d_cnt, d_self_of, d_toff, d_tdst, n_src, d_n_src, d_dh, s);
 }

@@ -123,6 +123,109 @@ def loss_and_grad(block: DeviceBlock, rows: torch.Tensor, labels: torch.Tensor,
     return loss, grads
 
 
+class GraphTrainer:
+    """The training step (model.py:107-146: forward, softmax cross-entropy,
+    analytic backward, SGD) of one sampler slot's batch b, captured once per
+    (slot buffers, b) as a CUDA graph and replayed for every later group that
+    lands in that slot.  The step reads the slot's live frontier sizes on the
+    device (the aggregation kernels' device counts; rows past them are zero
+    padding and the loss / gradients are masked to the live seeds), so a
+    replay needs no host sync and ~10 us of host time instead of ~150 eager
+    launches.  Parameters are updated in place (the same arithmetic as
+    sgd_step); the loss accumulates on the device.  Results equal the eager
+    step up to cuBLAS rounding on the padded GEMM shapes."""
+
+    def __init__(self, params: list[LayerParams], labels: torch.Tensor, feat_dim: int,
+                 num_nodes: int, lr: float):
+        self.params = [LayerParams(p.w_self.clone(), p.w_neigh.clone(), p.bias.clone())
+                       for p in params]
+        self.dtype = self.params[0].w_self.dtype
+        self.labels = labels
+        self.feat_dim = int(feat_dim)
+        self.n = int(num_nodes)
+        self.lr_t = torch.tensor(lr, dtype=self.dtype, device=labels.device)
+        self.loss_sum = torch.zeros((), dtype=torch.float64, device=labels.device)
+        self.rank = torch.empty(self.n, dtype=torch.int32, device=labels.device)
+        self.pool = torch.cuda.graph_pool_handle()
+        self.graphs: dict = {}
+        self.captures = 0
+
+    def _body(self, smp, rows_buf, b: int) -> None:
+        L, G = smp.L, smp.G
+        nf = smp.nfront
+        dn = [nf.data_ptr() + 4 * (d * G + b) for d in range(L + 1)]
+        front = [smp.front[d][b] for d in range(L + 1)]
+        rows = rows_buf[b, :, : self.feat_dim]
+        h = rows if self.dtype == torch.float32 else rows.to(self.dtype)
+        params = self.params
+        saved = []
+        for l, p in enumerate(params):
+            d = L - 1 - l
+            pos = sage_positions(front[d + 1], front[d], smp.ell[d][b], smp.cnt[d][b],
+                                 smp.step_fan[d], self.n, self.rank, dn[d + 1], dn[d])
+            mean, h_self = sage_mean(h, pos, smp.cnt[d][b], H=p.w_self.shape[0])
+            z = h_self @ p.w_self + mean @ p.w_neigh + p.bias
+            saved.append((h_self, mean, z, pos, d))
+            h = torch.clamp_min(z, 0) if l < L - 1 else z
+        cap0 = front[0].numel()
+        n0 = nf[0, b].to(self.dtype)
+        live = torch.arange(cap0, device=h.device) < nf[0, b]
+        y = self.labels[torch.where(live, front[0], 0).long()]
+        shifted = h - h.max(dim=1, keepdim=True).values
+        ex = torch.exp(shifted)
+        se = ex.sum(dim=1)
+        nll = -(shifted.gather(1, y[:, None])[:, 0] - torch.log(se))
+        loss = torch.where(live, nll, 0).sum() / n0
+        dz = ex / se[:, None]
+        dz.scatter_add_(1, y[:, None], -torch.ones((cap0, 1), dtype=dz.dtype, device=dz.device))
+        dz = torch.where(live[:, None], dz / n0, 0)
+        for l in range(L - 1, -1, -1):
+            p = params[l]
+            h_self, mean, z, pos, d = saved[l]
+            if l < L - 1:
+                dz = dz * (z > 0)
+            gws, gwn, gb = h_self.T @ dz, mean.T @ dz, dz.sum(dim=0)
+            if l > 0:
+                dself = dz @ p.w_self.T
+                dmean = dz @ p.w_neigh.T
+                dz = sage_mean_backward(dself, dmean, smp.cnt[d][b], pos)
+            p.w_self.sub_(self.lr_t * gws)
+            p.w_neigh.sub_(self.lr_t * gwn)
+            p.bias.sub_(self.lr_t * gb)
+        self.loss_sum.add_(loss.double())
+
+    def step(self, smp, rows_buf, b: int) -> None:
+        """One batch on the current stream (capturing its graph on first use)."""
+        key = (smp.front[0].data_ptr(), rows_buf.data_ptr(), int(b))
+        g = self.graphs.get(key)
+        if g is None:
+            cur = torch.cuda.current_stream()
+            if not self.graphs:
+                # first capture: let cuBLAS / the allocator initialise outside it,
+                # on a side stream, on throw-away copies of the parameters
+                keep = [LayerParams(p.w_self.clone(), p.w_neigh.clone(), p.bias.clone())
+                        for p in self.params]
+                loss0 = self.loss_sum.clone()
+                side = torch.cuda.Stream()
+                side.wait_stream(cur)
+                with torch.cuda.stream(side):
+                    self._body(smp, rows_buf, b)
+                cur.wait_stream(side)
+                for p, k in zip(self.params, keep):
+                    p.w_self.copy_(k.w_self)
+                    p.w_neigh.copy_(k.w_neigh)
+                    p.bias.copy_(k.bias)
+                self.loss_sum.copy_(loss0)
+            g = torch.cuda.CUDAGraph()
+            # thread_local: the GroupProducer thread keeps sampling / gathering
+            # on its own streams while this thread captures
+            with torch.cuda.graph(g, pool=self.pool, capture_error_mode="thread_local"):
+                self._body(smp, rows_buf, b)
+            self.graphs[key] = g
+            self.captures += 1
+        g.replay()
+
+
 def sgd_step(params: list[LayerParams], grads: list[LayerParams], lr: float) -> list[LayerParams]:
     lr_t = torch.tensor(lr, dtype=params[0].w_self.dtype, device=params[0].w_self.device)
     return [LayerParams(p.w_self - lr_t * g.w_self, p.w_neigh - lr_t * g.w_neigh,

@@ -400,11 +400,14 @@ class WorkerPipeline:
         # gather is faster (15.8 vs ~3.5 ms per launch)
         dense = ng * self.cap_in >= 4 * self.dg.n
         if self.gather_mode == "window" and dense and ng <= 128 and peer_mask == 0:
-            # id-window-major, straight from the group's input bitmaps
+            # staged union gather straight from the group's input bitmaps
+            self.gather_kernel = "gather_staged_kernel (rg_gather_window)"
             _lib.call("rg_gather_window", ptr(smp.bm), ptr(smp.wpre), self.dg.nwords, ng,
                       self.cap_in, ptr(route), bases_array(bases), st.src_stride, st.stride,
                       self.my_part, st.peer_mask, ptr(rows), cnt, _lib.stream_handle())
             return
+        self.gather_kernel = ("gather_queue_kernel (rg_gather_bundle)" if peer_mask == 0 else
+                              "gather_bundle_kernel<row-aligned> (rg_gather_bundle)")
         _lib.call("rg_gather_bundle", ptr(smp.front[smp.L]), ptr(smp.nfront[smp.L]), self.cap_in,
                   ng, ptr(route), bases_array(bases), st.src_stride, st.stride,
                   self.my_part, peer_mask, ptr(rows), cnt, _lib.stream_handle())

@@ -108,6 +108,7 @@ class RunConfig:
     prng: str = "splitmix"
     group: int = 16
     overlap: bool = True  # sample+gather group k+1 while group k trains (GroupProducer)
+    cuda_graphs: bool = True  # replay each slot/batch training step from a CUDA graph
 
     def validate(self) -> None:
         """train.py:121-135."""
@@ -205,6 +206,8 @@ def _run(cfg: RunConfig) -> list[WorkerResult]:
         records = []
         cache_keys = None
         secondary = None  # (thread, result dict) building epoch e+1's cache
+        trainer = (model.GraphTrainer(params, labels, g.feat_dim, g.num_nodes, cfg.lr)
+                   if cfg.cuda_graphs else None)
         for e in range(cfg.epochs):
             t0 = time.perf_counter()
             if rapid and (cfg.hot_scope == "epoch" or e == 0):
@@ -228,9 +231,15 @@ def _run(cfg: RunConfig) -> list[WorkerResult]:
                 secondary = _start_secondary(pipe, counts[e + 1], n_hot, max_count)
             pipe.start_epoch(sched, e)
             loss_sum = torch.zeros((), dtype=torch.float64, device=dg.device)
+            if trainer is not None:
+                loss_sum = trainer.loss_sum.clone()
 
             def train_group(smp, rows_buf, ng, nf):
                 nonlocal params
+                if trainer is not None:
+                    for b in range(ng):
+                        trainer.step(smp, rows_buf, b)
+                    return
                 for b in range(ng):
                     blk = model.block_from_slot(smp, b, nf[:, b])
                     rows = rows_buf[b, : int(nf[smp.L, b]), : g.feat_dim]
@@ -263,6 +272,9 @@ def _run(cfg: RunConfig) -> list[WorkerResult]:
                     if cfg.latency_ms > 0:
                         _sleep_rpcs(pipe, i0, ng, cfg.latency_ms)
                     train_group(smp, pipe.rows, ng, nf)
+            if trainer is not None:
+                loss_sum = trainer.loss_sum - loss_sum
+                params = trainer.params
             if secondary is not None:
                 secondary[0].join()  # the epoch includes the wait (train.py:233)
             t = pipe.totals()
