@@ -78,6 +78,30 @@ class DeviceGraph:
         self.max_degree = int(np.diff(np.asarray(indptr)).max()) if self.n else 0
 
     @classmethod
+    def from_device(cls, indptr: torch.Tensor, indices: torch.Tensor,
+                    num_nodes: int) -> "DeviceGraph":
+        """Adopt a CSR already in HBM (formats.load_graph_device): int64
+        indptr, int32 indices; row order and max degree found on the device."""
+        _lib.device()
+        dg = cls.__new__(cls)
+        dg.device = indptr.device
+        dg.n = int(num_nodes)
+        dg.nwords = (dg.n + 31) // 32
+        dg.indptr = indptr.contiguous()
+        dg.indices = indices.contiguous()
+        dg.num_edges = int(indices.numel())
+        deg = indptr[1:] - indptr[:-1]
+        dg.max_degree = int(deg.max().item()) if dg.n else 0
+        if dg.num_edges > 1:
+            dec = torch.nonzero(indices[1:] < indices[:-1]).flatten() + 1
+            start = torch.zeros(dg.num_edges + 1, dtype=torch.bool, device=dg.device)
+            start[indptr[1:-1]] = True
+            dg.sorted_rows = bool(start[dec].all().item()) if dec.numel() else True
+        else:
+            dg.sorted_rows = True
+        return dg
+
+    @classmethod
     def of(cls, g) -> "DeviceGraph":
         """Device copy of a Graph (ours or the reference's), cached on it."""
         cached = getattr(g, "_rg_device", None)

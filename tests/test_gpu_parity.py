@@ -928,3 +928,55 @@ def test_group_prefetch_pipeline_single_gpu(rg, products):
         ref.step(i0)
     r = ref.totals()
     assert t["bad"] == 0 and np.array_equal(t["per_batch"][:128, :5], r["per_batch"][:128, :5])
+
+
+def test_rgf1_rpb1_straight_to_device(rg, tmp_path):
+    """formats.load_graph_device / load_partition_device (graph.py:219-290,
+    partition.py:97-119 layouts): the file's sections land in HBM equal to
+    the host loader's arrays; a sampling run on the loaded CSR equals the
+    oracle; the reference's error classes for corrupt files."""
+    from paper_2505_10806_b200 import formats
+    from paper_2505_10806_b200.graph import GraphFormatError, GraphValidationError
+
+    g = rg.synth_powerlaw(3000, 4, 12, 5, seed=7)
+    book = rg.partition_edgecut(g, 3)
+    gp, pp = tmp_path / "g.rgf1", tmp_path / "p.rpb1"
+    rg.save_graph(g, gp)
+    rg.save_partition(book, pp)
+    dev = formats.load_graph_device(gp)
+    assert torch.equal(dev.graph.indptr.cpu(), torch.from_numpy(g.indptr.astype(np.int64)))
+    assert torch.equal(dev.graph.indices.cpu(), torch.from_numpy(g.indices.astype(np.int32)))
+    assert torch.equal(dev.features.cpu(), torch.from_numpy(g.features))
+    assert torch.equal(dev.labels.cpu(), torch.from_numpy(g.labels.astype(np.int64)))
+    for m, want in ((dev.train_mask, g.train_mask), (dev.val_mask, g.val_mask),
+                    (dev.test_mask, g.test_mask)):
+        assert torch.equal(m.cpu(), torch.from_numpy(want))
+    assert dev.graph.sorted_rows and dev.graph.max_degree == int(np.diff(g.indptr).max())
+    k, owner = formats.load_partition_device(pp)
+    assert k == 3 and torch.equal(owner.cpu(), torch.from_numpy(book.owner.astype(np.uint8)))
+    # the device CSR drives the sampler directly
+    from paper_2505_10806_b200.engine import BlockSampler
+
+    smp = BlockSampler(dev.graph, [5, 4], 64, group=1)
+    seeds = np.flatnonzero(g.train_mask)[:64]
+    smp.set_seeds(0, seeds, 11)
+    smp.run(1)
+    fr, _ = orc.block(g.indptr, g.indices, seeds, [5, 4], 11)
+    n = int(smp.nfront[2, 0].item())
+    assert np.array_equal(smp.front[2][0, :n].cpu().numpy(), fr[-1])
+    # corrupt files
+    raw = gp.read_bytes()
+    bad = tmp_path / "bad.rgf1"
+    bad.write_bytes(b"XXXX" + raw[4:])
+    with pytest.raises(GraphFormatError):
+        formats.load_graph_device(bad)
+    bad.write_bytes(raw[:-10])
+    with pytest.raises(OSError):
+        formats.load_graph_device(bad)
+    arr = bytearray(raw)
+    hdr = 4 + 4 + 8 + 8 + 4 + 4
+    arr[hdr + 8 * (g.num_nodes + 1): hdr + 8 * (g.num_nodes + 1) + 8] = \
+        (10**9).to_bytes(8, "little")  # first neighbour id out of range
+    bad.write_bytes(bytes(arr))
+    with pytest.raises(GraphValidationError):
+        formats.load_graph_device(bad)
