@@ -296,6 +296,9 @@ __global__ void __launch_bounds__(kGatherWarps * 32, 4)
 // kWinWords words (128 ids, ~34 rows at Products density) of one batch.
 constexpr int kWinWords = 4;  // item = 4 bitmap words (128 ids) of one batch
 constexpr unsigned kWordClaim = 4;
+#ifndef RG_STAGED_MIN_CTAS
+#define RG_STAGED_MIN_CTAS 4
+#endif
 
 __global__ void __launch_bounds__(kGatherWarps * 32, 4)
     gather_window_kernel(const uint32_t* __restrict__ bm, const int32_t* __restrict__ wpre,
@@ -444,7 +447,7 @@ __global__ void __launch_bounds__(kGatherWarps * 32, 4)
 // too but scatters 400-B writes over all G bundles at once and measured
 // 11.7 ms: HBM write locality matters more than the reads.)
 template <int kW>
-__global__ void __launch_bounds__(kGatherWarps * 32)
+__global__ void __launch_bounds__(kGatherWarps * 32, RG_STAGED_MIN_CTAS)
     gather_staged_kernel(const uint32_t* __restrict__ bm, const int32_t* __restrict__ wpre,
                          int64_t nwords, int G, int64_t cap, const uint32_t* __restrict__ route,
                          const __grid_constant__ Bases bases, int src_stride, int stride,

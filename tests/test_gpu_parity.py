@@ -980,3 +980,48 @@ def test_rgf1_rpb1_straight_to_device(rg, tmp_path):
     bad.write_bytes(bytes(arr))
     with pytest.raises(GraphValidationError):
         formats.load_graph_device(bad)
+
+
+def test_products_overlapped_producer_consumer_race_free(products):
+    """The concurrent path end to end at Products scale: the GroupProducer
+    thread samples / gathers group k+1 into the other slot while the
+    consumer stream checks group k — every batch's bundle rows against the
+    feature rows of its input nodes, on the device, with no host sync in the
+    loop — then releases the slot for reuse.  Cross-stream slot reuse or a
+    missing event would show up as mismatched rows; the per-batch accounting
+    must equal a serial run's.  (compute-sanitizer is closed on this pool.)"""
+    from paper_2505_10806_b200.pipeline import GroupProducer, WorkerPipeline
+    from paper_2505_10806_b200.sampler import SeedSchedule
+
+    g, dg, store = products
+    d = g.feat_dim
+    feats = torch.from_numpy(g.features).cuda()
+    train = np.flatnonzero(g.train_mask)
+    pipe = WorkerPipeline(dg, store, 0, train, [15, 10, 5], 1024, 7, 64, nbuf=2)
+    sched = SeedSchedule(7, 1, pipe.nb)
+    pipe.start_epoch(sched, 0)
+    bad = torch.zeros((), dtype=torch.int64, device="cuda")
+    checked = torch.zeros((), dtype=torch.int64, device="cuda")
+    prod = GroupProducer(pipe, range(0, pipe.nb, pipe.G))
+    try:
+        while (item := prod.next_group()) is not None:
+            i0, ng, slot, nf = item
+            smp, rows = pipe.samplers[slot], pipe.row_bufs[slot]
+            L = smp.L
+            valid = (torch.arange(smp.caps[L], device="cuda")[None, :]
+                     < smp.nfront[L, :ng].long()[:, None])
+            ids = smp.front[L][:ng].long()[valid]
+            bad += (rows[:ng, :, :d][valid] != feats[ids]).any(dim=1).sum()
+            checked += valid.sum()
+            prod.release(slot)
+    finally:
+        prod.close()
+    torch.cuda.synchronize()
+    conc = pipe.totals()
+    assert int(bad.item()) == 0
+    assert int(checked.item()) == 1_126_570_328  # every input row of the epoch
+    ref = WorkerPipeline(dg, store, 0, train, [15, 10, 5], 1024, 7, 64, nbuf=1)
+    ref.start_epoch(sched, 0)
+    for i0 in range(0, ref.nb, ref.G):
+        ref.step(i0)
+    assert np.array_equal(conc["per_batch"][:, :5], ref.totals()["per_batch"][:, :5])
