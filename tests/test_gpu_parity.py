@@ -997,7 +997,7 @@ def test_products_overlapped_producer_consumer_race_free(products):
     d = g.feat_dim
     feats = torch.from_numpy(g.features).cuda()
     train = np.flatnonzero(g.train_mask)
-    pipe = WorkerPipeline(dg, store, 0, train, [15, 10, 5], 1024, 7, 64, nbuf=2)
+    pipe = WorkerPipeline(dg, store, 0, train, [15, 10, 5], 1024, 7, 32, nbuf=2)
     sched = SeedSchedule(7, 1, pipe.nb)
     pipe.start_epoch(sched, 0)
     bad = torch.zeros((), dtype=torch.int64, device="cuda")
@@ -1020,7 +1020,7 @@ def test_products_overlapped_producer_consumer_race_free(products):
     conc = pipe.totals()
     assert int(bad.item()) == 0
     assert int(checked.item()) == 1_126_570_328  # every input row of the epoch
-    ref = WorkerPipeline(dg, store, 0, train, [15, 10, 5], 1024, 7, 64, nbuf=1)
+    ref = WorkerPipeline(dg, store, 0, train, [15, 10, 5], 1024, 7, 32, nbuf=1)
     ref.start_epoch(sched, 0)
     for i0 in range(0, ref.nb, ref.G):
         ref.step(i0)
