@@ -9,6 +9,7 @@ expansion).  Results are bit-identical to the reference.
 from __future__ import annotations
 
 import threading
+from collections.abc import Sequence
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -65,6 +66,37 @@ def epoch_batches(train_nodes: np.ndarray, batch_size: int, s: SeedSchedule,
     return [perm[i: i + batch_size] for i in range(0, len(perm), batch_size)]
 
 
+class DeviceEdges(Sequence):
+    """edges[d] = (src, dst) int64 arrays, copied from the device on first
+    access: the flat (dst, src)-sorted edge lists are built on the device when
+    the block is made (rg_ell_to_edges, fresh buffers) and stay there until a
+    host consumer reads them — the reference's Prefetcher consumer reads only
+    the bundle rows, the device model reads the ELL form."""
+
+    def __init__(self, parts: list, L: int):
+        self._parts = parts  # [(src view, dst view)] device int32, per level
+        self._L = L
+        self._host = None
+
+    def _get(self):
+        if self._host is None:
+            flat = torch.cat([t for pair in self._parts for t in pair])
+            host = torch.empty(flat.shape, dtype=flat.dtype, pin_memory=True)
+            host.copy_(flat)
+            out = host.numpy().astype(np.int64)
+            cuts = np.cumsum([int(t.numel()) for pair in self._parts for t in pair])[:-1]
+            pieces = np.split(out, cuts)
+            self._host = [(pieces[2 * d], pieces[2 * d + 1]) for d in range(self._L)]
+            self._parts = None
+        return self._host
+
+    def __len__(self) -> int:
+        return self._L
+
+    def __getitem__(self, i):
+        return self._get()[i]
+
+
 @dataclass
 class ComputationBlock:
     """Layered subgraph of one mini-batch (sampler.py:60-83).
@@ -112,8 +144,8 @@ def _sampler_for(dg: DeviceGraph, fanouts, n_seeds: int, prng: str = "splitmix")
 def block_from_sampler(smp: BlockSampler, slot: int, seeds: np.ndarray, epoch: int,
                        batch: int) -> ComputationBlock:
     """Materialise slot `slot` of a sampler run as a numpy ComputationBlock:
-    flat edges per level on the device, one D2H of the sizes, one packed D2H
-    of every frontier and edge array."""
+    flat edges per level built on the device (kept there until read, see
+    DeviceEdges), one D2H of the sizes, one packed D2H of the frontiers."""
     L = smp.L
     lv = [smp.edges(d, slot + 1) for d in range(L)]
     sizes = torch.cat([smp.nfront[:, slot]] + [e[2][slot:slot + 1] for e in lv]).cpu().numpy()
@@ -122,16 +154,13 @@ def block_from_sampler(smp: BlockSampler, slot: int, seeds: np.ndarray, epoch: i
         if nf[d] > smp.caps[d]:
             raise RuntimeError(f"frontier {d} overflow ({nf[d]} > {smp.caps[d]})")
     parts = [smp.front[d][slot, : nf[d]] for d in range(L + 1)]
-    for d in range(L):
-        parts += [lv[d][0][slot, : ne[d]], lv[d][1][slot, : ne[d]]]
     flat = torch.cat(parts)
     host = torch.empty(flat.shape, dtype=flat.dtype, pin_memory=True)
     host.copy_(flat)
     out = host.numpy().astype(np.int64)
-    cuts = np.cumsum([int(p.numel()) for p in parts])[:-1]
-    pieces = np.split(out, cuts)
-    frontiers = pieces[:L + 1]
-    edges = [(pieces[L + 1 + 2 * d], pieces[L + 2 + 2 * d]) for d in range(L)]
+    frontiers = np.split(out, np.cumsum([int(p.numel()) for p in parts])[:-1])
+    edges = DeviceEdges([(lv[d][0][slot, : ne[d]], lv[d][1][slot, : ne[d]]) for d in range(L)],
+                        L)
     input_dev = parts[L].clone()
     return ComputationBlock(epoch=epoch, batch=batch, seeds=seeds, frontiers=frontiers,
                             edges=edges, device={"input_nodes": input_dev})
