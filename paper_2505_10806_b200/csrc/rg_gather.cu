@@ -542,44 +542,41 @@ __global__ void __launch_bounds__(kGatherWarps * 32, RG_STAGED_MIN_CTAS)
       }
     }
     __syncthreads();
-    // phase 2: each batch's run of the window, contiguous
-    const uint32_t fbk = s_fbkinds;
+    // phase 2a: provenance of the window for this warp's batches, one batch
+    // per lane (batch w + 8l belongs to lane l of warp w in every window, so
+    // the CTA's per-batch counters need no atomics)
+    {
+      const int bb = warp + kGatherWarps * lane;
+      if (bb < G) {
+        const uint32_t fbk = s_fbkinds;
+        unsigned n_loc = 0, n_hit = 0, n_fb = 0, n_bad = 0, n_peer = 0, om = 0;
+#pragma unroll
+        for (int q = 0; q < kW; ++q) {
+          const uint32_t word = s_words[bb * kW + q];
+          n_loc += __popc(word & s_mloc[q]);
+          n_hit += __popc(word & s_mhit[q]);
+          n_fb += __popc(word & s_mfb[q]);
+          n_bad += __popc(word & s_mbad[q]);
+          n_peer += __popc(word & s_mpeer[q]);
+          for (unsigned kk = fbk; kk; kk &= kk - 1) {
+            const int kq = __ffs(kk) - 1;
+            if (word & s_mq[kq][q]) om |= 1u << kq;
+          }
+        }
+        uint32_t* sc = s_cnt[bb];
+        sc[RG_CNT_LOCAL] += n_loc;
+        sc[RG_CNT_HIT] += n_hit;
+        sc[RG_CNT_FALLBACK] += n_fb;
+        sc[RG_CNT_BAD] += n_bad;
+        sc[RG_CNT_PEER] += n_peer;
+        sc[RG_CNT_OWNER_MASK] |= om;
+      }
+    }
+    // phase 2b: each batch's run of the window, contiguous
     for (int bb = warp; bb < G; bb += kGatherWarps) {
       const uint32_t wd = lane < kW ? s_words[bb * kW + lane] : 0u;
-      int pre = __popc(wd);
-#pragma unroll
-      for (int o = 1; o < kW; o <<= 1) {
-        const int y = __shfl_up_sync(kFull, pre, o);
-        if (lane >= o) pre += y;
-      }
-      const int m = __shfl_sync(kFull, pre, kW - 1);
-      if (m == 0) continue;
-      pre -= __popc(wd);
+      if (__reduce_or_sync(kFull, wd) == 0u) continue;
       const int base = s_rbase[bb];
-      unsigned n_loc = 0, n_hit = 0, n_fb = 0, n_bad = 0, n_peer = 0, om = 0;
-#pragma unroll
-      for (int q = 0; q < kW; ++q) {
-        const uint32_t word = __shfl_sync(kFull, wd, q);
-        n_loc += __popc(word & s_mloc[q]);
-        n_hit += __popc(word & s_mhit[q]);
-        n_fb += __popc(word & s_mfb[q]);
-        n_bad += __popc(word & s_mbad[q]);
-        n_peer += __popc(word & s_mpeer[q]);
-        for (unsigned kk = fbk; kk; kk &= kk - 1) {
-          const int kq = __ffs(kk) - 1;
-          if (word & s_mq[kq][q]) om |= 1u << kq;
-        }
-      }
-      if (lane == 0) {
-        uint32_t* sc = s_cnt[bb];
-        if (n_loc) atomicAdd(sc + RG_CNT_LOCAL, n_loc);
-        if (n_hit) atomicAdd(sc + RG_CNT_HIT, n_hit);
-        if (n_fb) atomicAdd(sc + RG_CNT_FALLBACK, n_fb);
-        if (n_bad) atomicAdd(sc + RG_CNT_BAD, n_bad);
-        if (n_peer) atomicAdd(sc + RG_CNT_PEER, n_peer);
-        if (om) atomicOr(sc + RG_CNT_OWNER_MASK, om);
-      }
-      __syncwarp();
       // the batch's rows in id order = consecutive output rows; four rows per
       // step, lane c moves vector c of each (no per-element index math)
       float4* dst = reinterpret_cast<float4*>(out + ((int64_t)bb * cap + base) * stride);
