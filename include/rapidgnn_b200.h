@@ -197,6 +197,11 @@ int rg_gather_window(const uint32_t* d_bm, const int32_t* d_wpre, int64_t nwords
                      int32_t src_stride, int32_t stride, int32_t my_part, uint32_t peer_mask,
                      float* d_out, uint32_t* d_counters, void* stream);
 
+/* Copy nbytes from d_src to d_dst on the stream's copy engine (either
+ * address may be a peer GPU's IPC mapping): the whole-shard form of the
+ * group prefetch for dense groups.                                       */
+int rg_copy_bytes(void* d_dst, const void* d_src, int64_t nbytes, void* stream);
+
 /* ---- group prefetch of peer rows (north_star item 4) ---
  * bits[w] bit j = the route kind of node 32w+j is in kind_mask.         */
 int rg_route_kind_bits(const uint32_t* d_route, int64_t n, uint32_t kind_mask, uint32_t* d_bits,

@@ -62,6 +62,7 @@ _SIGNATURES = {
                                    c_uint32, P, P, P]),
     "rg_gather_window": (c_int32, [P, P, c_int64, c_int32, c_int64, P, P, c_int32, c_int32,
                                    c_int32, c_uint32, P, P, P]),
+    "rg_copy_bytes": (c_int32, [P, P, c_int64, P]),
     "rg_route_kind_bits": (c_int32, [P, c_int64, c_uint32, P, P]),
     "rg_group_union": (c_int32, [P, c_int64, c_int32, P, P, P]),
     "rg_prefetch_rows": (c_int32, [P, P, c_int64, P, P, P, c_int32, c_int32, P]),

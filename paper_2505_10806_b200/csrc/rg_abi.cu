@@ -124,6 +124,18 @@ extern "C" int rg_enable_peer(int32_t peer) {
   return RG_OK;
 }
 
+// bytes from src to dst (either may be a peer GPU's IPC-mapped address) on the
+// copy engines: the dense-group prefetch copies whole peer shards this way
+// (one cudaMemcpyAsync per shard, no SMs used)
+extern "C" int rg_copy_bytes(void* d_dst, const void* d_src, int64_t nbytes, void* stream) {
+  RG_REQUIRE(nbytes >= 0 && (nbytes == 0 || (d_dst && d_src)), "rg_copy_bytes: bad arguments");
+  if (nbytes == 0) return RG_OK;
+  if (cudaMemcpyAsync(d_dst, d_src, (size_t)nbytes, cudaMemcpyDefault, (cudaStream_t)stream) !=
+      cudaSuccess)
+    return rg::check_launch("rg_copy_bytes");
+  return RG_OK;
+}
+
 // host forms of the PRNG variants (for known-answer tests against the oracle)
 extern "C" int rg_prng_raw(int32_t kind, uint64_t k0, uint64_t k1, int64_t count, uint64_t* out) {
   using namespace rg;

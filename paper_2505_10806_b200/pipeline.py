@@ -137,6 +137,7 @@ class WorkerPipeline:
         self.pf_ids = torch.empty(st.n, dtype=I32, device=dev)
         self.pf_n = torch.zeros(self.nbuf, dtype=I32, device=dev)
         self.pf_rows = torch.zeros(1, dtype=torch.int64, device=dev)  # rows copied (stats)
+        self.pf_whole_shards = os.environ.get("RG_PREFETCH_WHOLE", "1") != "0"
         self.prefetch = bool(peers)
 
     def _route(self):
@@ -157,6 +158,16 @@ class WorkerPipeline:
             self._exchange_nccl(ng, smp, slot, route, dst)
             self.pf_rows += self.pf_n[slot]
             self.launches += 6
+            return
+        if self.pf_whole_shards and ng * self.cap_in >= 4 * self.dg.n:
+            # dense group: its union of peer rows is nearly every row of the
+            # peer shards (Products G = 128: 1.03 M of 1.22 M at N = 2), so the
+            # shards are copied whole on the copy engines (contiguous, ~820 GB/s
+            # measured, no SMs) instead of gathered row by row (~540 GB/s)
+            for q, t in self.shadow[slot].items():
+                _lib.call("rg_copy_bytes", t.data_ptr(), st.bases[q], t.numel() * 4, s)
+                self.pf_rows += t.shape[0]
+            self.launches += len(self.shadow[slot])
             return
         _lib.call("rg_route_kind_bits", ptr(route), st.n, st.peer_mask, ptr(self.pf_mask), s)
         _lib.call("rg_group_union", ptr(smp.bm), nw, ng, ptr(self.pf_mask), ptr(self.pf_union), s)
