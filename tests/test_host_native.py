@@ -348,3 +348,24 @@ def test_device_path_has_no_cpu_fallback(monkeypatch):
     monkeypatch.setattr(_lib, "LIB_PATH", ROOT / "does_not_exist.so")
     with pytest.raises(_lib.ExtensionMissing):
         _lib.load()
+
+
+def test_reference_arm_runs_without_the_product_library():
+    """bench.py --impl reference: the reference's CPU path on the host cores,
+    inputs from the C oracle (hash-pinned), the worker-0 hot set, and the
+    same `config` keys as the B200 arm; it asserts that neither the product
+    package nor librapidgnn_b200.so was loaded before printing its line."""
+    import json
+    import subprocess
+    import sys
+
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference",
+                          "--config", "c1", "--steps", "1", "--warmup", "1"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([x for x in out.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert set(line["config"]) == {"workload", "batch_size", "fanouts", "partitions", "worker",
+                                   "cache_pct", "n_hot", "prng"}
+    assert line["config"]["n_hot"] == 7125  # int(15 % of worker 0's C1 remote nodes)
+    assert line["cpu_baseline"]["kind"] == "port"
