@@ -607,8 +607,10 @@ def main():
     n_batches = len(timed_batches)
     # our kernels per step: fill_seeds, mark_seeds, 2 compaction, per level
     # (node_meta, sample_level, 2 compaction), gather; + 5 for the group
-    # prefetch (kind bits, union, 2 compaction, row copy) when enabled
-    gpu_launches = args.steps * (5 + 4 * smp.L + (5 if pipe.prefetch else 0))
+    # prefetch (kind bits, union, 2 compaction, row copy) when it gathers rows
+    # (dense groups copy whole shards with cudaMemcpyAsync: no kernels)
+    pf_kernels = 5 if pipe.prefetch and getattr(pipe, "pf_mode", "rows") == "rows" else 0
+    gpu_launches = args.steps * (5 + 4 * smp.L + pf_kernels)
 
     # full-epoch accounting pass (remote rows/epoch, parity metric)
     pipe.start_epoch(sched, 0)
@@ -723,8 +725,11 @@ def main():
         "e2e": e2e,
         "e2e_host_rows": e2e_rows,
         **legs,
-        "nvlink": ({"mode": ("group prefetch (rg_prefetch_rows): each group's peer rows "
-                             "copied once into local shadows, gather all-local"
+        "nvlink": ({"mode": (("group prefetch: the peer shards copied whole on the copy "
+                              "engines (dense group, rg_copy_bytes), gather all-local"
+                              if getattr(pipe, "pf_mode", "rows") != "rows" else
+                              "group prefetch (rg_prefetch_rows): each group's peer rows "
+                              "copied once into local shadows, gather all-local")
                              if args.transport == "p2p" else
                              "group prefetch over NCCL all-to-all (ids out, rows back, "
                              "rg_scatter_rows into local shadows), gather all-local"),

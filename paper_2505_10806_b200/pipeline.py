@@ -167,8 +167,9 @@ class WorkerPipeline:
             for q, t in self.shadow[slot].items():
                 _lib.call("rg_copy_bytes", t.data_ptr(), st.bases[q], t.numel() * 4, s)
                 self.pf_rows += t.shape[0]
-            self.launches += len(self.shadow[slot])
+            self.pf_mode = "whole shards"
             return
+        self.pf_mode = "rows"
         _lib.call("rg_route_kind_bits", ptr(route), st.n, st.peer_mask, ptr(self.pf_mask), s)
         _lib.call("rg_group_union", ptr(smp.bm), nw, ng, ptr(self.pf_mask), ptr(self.pf_union), s)
         _lib.call("rg_bitmap_compact", ptr(self.pf_union), nw, 1, ptr(self.pf_chunk),
