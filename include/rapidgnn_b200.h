@@ -184,14 +184,16 @@ int rg_gather_bundle(const int32_t* d_ids, const int32_t* d_nids, int64_t cap, i
                      int32_t stride, int32_t my_part, uint32_t peer_mask, float* d_out,
                      uint32_t* d_counters, void* stream);
 
-/* The same gather driven by the group's input bitmaps instead of id lists:
- * d_bm [G x nwords] (bit j of word w set <=> node 32w+j is in batch b's
- * input set, the sampler's level-L bitmaps) and d_wpre [G x nwords] (rank of
- * node 32w in batch b's sorted set, rg_bitmap_compact's d_wpre); row r of
- * batch b's bundle (the r-th smallest input node) goes to d_out + (b*cap +
- * r)*stride.  Work runs id-window-major (word w of every batch together), so
- * rows shared by the group's batches are read from HBM about once.  Same
- * route / bases / counters contract as rg_gather_bundle; G <= 128.        */
+/* The same gather for a whole group, driven by the group's input bitmaps
+ * instead of id lists: d_bm [G x nwords] (bit j of word w set <=> node
+ * 32w+j is in batch b's input set, the sampler's level-L bitmaps) and d_wpre
+ * [G x nwords] (rank of node 32w in batch b's sorted set, rg_bitmap_compact's
+ * d_wpre); row r of batch b's bundle (the r-th smallest input node) goes to
+ * d_out + (b*cap + r)*stride.  A CTA stages each present source row of a
+ * 64-id window once in shared memory and writes every batch's run of the
+ * window contiguously, so rows shared by the group's batches are read from
+ * HBM once per group.  Same route / bases / counters contract as
+ * rg_gather_bundle; G <= 128, rows up to ~1.5 K floats.                  */
 int rg_gather_window(const uint32_t* d_bm, const int32_t* d_wpre, int64_t nwords, int32_t G,
                      int64_t cap, const uint32_t* d_route, const float* const* h_bases,
                      int32_t src_stride, int32_t stride, int32_t my_part, uint32_t peer_mask,

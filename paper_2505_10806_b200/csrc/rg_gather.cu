@@ -282,156 +282,14 @@ __global__ void __launch_bounds__(kGatherWarps * 32, 4)
   }
 }
 
-// ---- window-major gather from the input bitmaps ----------------------------
-// The group's input sets as the sampler leaves them: bm[b][w] (bit j of word w
-// = node 32w+j is in batch b's input set) and wpre[b][w] (rank of node 32w in
-// that sorted set).  Work items k = w*G + b — id-window-major: every batch's
-// rows for the same 32 ids are copied around the same time, so each source
-// row is read from HBM about once and then served from L2 to the group's
-// other batches (the rank-major queue above lets batches drift apart in id
-// space by up to ~10^4 ids, far enough that the bundle write stream evicts
-// the shared rows in between: DRAM reads 5.2 GB per G = 128 launch against
-// 2.5 GB here).  No id list is read: a window's set bits give the ids, its
-// wpre entry the output rank of its first row.  Items are windows of
-// kWinWords words (128 ids, ~34 rows at Products density) of one batch.
-constexpr int kWinWords = 4;  // item = 4 bitmap words (128 ids) of one batch
-constexpr unsigned kWordClaim = 4;
+// ---- group gather from the input bitmaps -----------------------------------
+// The group's input sets as the sampler leaves them: bm[b][w] (bit j of word
+// w = node 32w+j is in batch b's input set) and wpre[b][w] (rank of node 32w
+// in that sorted set).  No id list is read: a window's set bits give the
+// ids, its wpre entry the output rank of its first row.
 #ifndef RG_STAGED_MIN_CTAS
 #define RG_STAGED_MIN_CTAS 4
 #endif
-
-__global__ void __launch_bounds__(kGatherWarps * 32, 4)
-    gather_window_kernel(const uint32_t* __restrict__ bm, const int32_t* __restrict__ wpre,
-                         int64_t nwords, int G, int64_t cap, const uint32_t* __restrict__ route,
-                         const __grid_constant__ Bases bases, int src_stride, int stride,
-                         int nvec, int dq, int dr, int my_part, uint32_t peer_mask,
-                         float* __restrict__ out, uint32_t* __restrict__ counters,
-                         unsigned* __restrict__ queue) {
-  __shared__ uint32_t s_cnt[kQueueMaxG][RG_NCOUNTERS];
-  __shared__ const float* s_base[16];
-  __shared__ unsigned long long s_src[kGatherWarps][32 * kWinWords];
-  const int lane = lane_id();
-  const int warp = threadIdx.x >> 5;
-  const unsigned lt = (1u << lane) - 1u;
-  for (int i = threadIdx.x; i < kQueueMaxG * RG_NCOUNTERS; i += blockDim.x)
-    (&s_cnt[0][0])[i] = 0;
-  if (threadIdx.x < 16) s_base[threadIdx.x] = bases.p[threadIdx.x];
-  __syncthreads();
-  unsigned long long* srcw = s_src[warp];
-  const int64_t nwin = (nwords + kWinWords - 1) / kWinWords;
-  const unsigned items = (unsigned)nwin * (unsigned)G;
-  for (;;) {
-    unsigned t0 = 0;
-    if (lane == 0) t0 = atomicAdd(queue, kWordClaim);
-    t0 = __shfl_sync(kFull, t0, 0);
-    if (t0 >= items) break;
-    int64_t win = t0 / (unsigned)G;  // one division per claim
-    int b = (int)(t0 - (unsigned)win * (unsigned)G) - 1;
-#pragma unroll 1
-    for (unsigned k = t0; k < t0 + kWordClaim && k < items; ++k) {
-      if (++b == G) {
-        b = 0;
-        ++win;
-      }
-      // the window's words (lanes 0..3) and their exclusive bit prefix
-      const int64_t w0 = win * kWinWords;
-      const int64_t wl = w0 + lane;
-      const uint32_t wd = (lane < kWinWords && wl < nwords) ? __ldg(bm + (int64_t)b * nwords + wl)
-                                                           : 0u;
-      int pre = __popc(wd);
-#pragma unroll
-      for (int o = 1; o < kWinWords; o <<= 1) {
-        const int y = __shfl_up_sync(kFull, pre, o);
-        if (lane >= o) pre += y;
-      }
-      const int m = __shfl_sync(kFull, pre, kWinWords - 1);
-      if (m == 0) continue;
-      pre -= __popc(wd);  // exclusive
-      const int base = __ldg(wpre + (int64_t)b * nwords + w0);
-      // bit lanes: route, provenance, source address into the row's slot
-      uint32_t rt[kWinWords], word[kWinWords];
-#pragma unroll
-      for (int q = 0; q < kWinWords; ++q) {
-        word[q] = __shfl_sync(kFull, wd, q);
-        rt[q] = ((word[q] >> lane) & 1u) ? __ldg(route + ((w0 + q) * 32 + lane)) : RG_ROUTE_INVALID;
-      }
-      unsigned n_local = 0, n_hit = 0, n_fb = 0, n_bad = 0, n_peer = 0, om = 0;
-#pragma unroll
-      for (int q = 0; q < kWinWords; ++q) {
-        const bool set = (word[q] >> lane) & 1u;
-        const int kind = (int)(rt[q] >> RG_KIND_SHIFT);
-        const float* bp = (set && rt[q] != RG_ROUTE_INVALID) ? s_base[kind] : nullptr;
-        const bool bad = set && bp == nullptr;
-        const bool local = set && !bad && kind == my_part;
-        const bool hit = set && !bad && kind == (int)RG_KIND_CACHE;
-        const bool fb = set && !bad && !local && !hit;
-        n_local += __popc(__ballot_sync(kFull, local));
-        n_hit += __popc(__ballot_sync(kFull, hit));
-        n_fb += __popc(__ballot_sync(kFull, fb));
-        n_bad += __popc(__ballot_sync(kFull, bad));
-        n_peer += __popc(__ballot_sync(kFull, fb && ((peer_mask >> kind) & 1u)));
-        om |= __reduce_or_sync(kFull, fb ? (1u << kind) : 0u);
-        const int off = __shfl_sync(kFull, pre, q);
-        if (set)
-          srcw[off + __popc(word[q] & lt)] = reinterpret_cast<unsigned long long>(
-              bp ? bp + (int64_t)(rt[q] & RG_ROW_MASK) * src_stride : nullptr);
-      }
-      if (lane == 0) {
-        uint32_t* sc = s_cnt[b];
-        if (n_local) atomicAdd(sc + RG_CNT_LOCAL, n_local);
-        if (n_hit) atomicAdd(sc + RG_CNT_HIT, n_hit);
-        if (n_fb) atomicAdd(sc + RG_CNT_FALLBACK, n_fb);
-        if (n_bad) atomicAdd(sc + RG_CNT_BAD, n_bad);
-        if (n_peer) atomicAdd(sc + RG_CNT_PEER, n_peer);
-        if (om) atomicOr(sc + RG_CNT_OWNER_MASK, om);
-      }
-      __syncwarp();
-      float4* dst = reinterpret_cast<float4*>(out + ((int64_t)b * cap + base) * stride);
-      const int total = m * nvec;
-      int er = lane / nvec, ec = lane - (lane / nvec) * nvec;
-      for (int e0 = 0; e0 < total; e0 += 32 * kUnroll) {
-        float4 v[kUnroll];
-        int rr[kUnroll], cc[kUnroll];
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          rr[u] = er;
-          cc[u] = ec;
-          ec += dr;
-          er += dq;
-          if (ec >= nvec) {
-            ec -= nvec;
-            ++er;
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          const int e = e0 + u * 32 + lane;
-          const unsigned long long sp = e < total ? srcw[rr[u]] : 0ull;
-          v[u] = sp ? ld_stream(reinterpret_cast<const float4*>(sp) + cc[u])
-                    : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          const int e = e0 + u * 32 + lane;
-          if (e < total) st_stream(dst + e, v[u]);
-        }
-      }
-      __syncwarp();  // srcw is rewritten by the next item
-    }
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < G * RG_NCOUNTERS; i += blockDim.x) {
-    const int bb = i / RG_NCOUNTERS, k = i - bb * RG_NCOUNTERS;
-    const uint32_t x = s_cnt[bb][k];
-    if (x) {
-      uint32_t* g = counters + (int64_t)bb * RG_NCOUNTERS + k;
-      if (k == RG_CNT_OWNER_MASK)
-        atomicOr(g, x);
-      else
-        atomicAdd(g, x);
-    }
-  }
-}
 
 // ---- staged union gather: each source row read once per group -------------
 // The window kernel above still moves every bundle row through L2 twice (the
@@ -735,8 +593,7 @@ extern "C" int rg_gather_window(const uint32_t* d_bm, const int32_t* d_wpre, int
                                 uint32_t* d_counters, void* stream) {
   RG_REQUIRE(G >= 1 && G <= kQueueMaxG && cap >= 1 && nwords >= 1,
              "rg_gather_window: bad sizes (G <= %d)", kQueueMaxG);
-  RG_REQUIRE((uint64_t)G * (uint64_t)nwords < (1ull << 32) - kWordClaim,
-             "rg_gather_window: G * nwords above the 32-bit work queue");
+  RG_REQUIRE(nwords < (1ll << 32) - 1, "rg_gather_window: too many bitmap words");
   RG_REQUIRE(stride >= 4 && stride % 4 == 0, "rg_gather_window: stride %d not a multiple of 4",
              stride);
   RG_REQUIRE(src_stride >= stride && src_stride % 4 == 0,
@@ -752,18 +609,6 @@ extern "C" int rg_gather_window(const uint32_t* d_bm, const int32_t* d_wpre, int
   const int dq = 32 / nvec, dr = 32 % nvec;
   unsigned* q = queue_slot((cudaStream_t)stream);
   if (!q) return check_launch("gather window queue");
-  // 4 CTAs/SM (58 registers: the whole register file): gather alone 6.51 ms
-  // at 3 or 4 per SM (Products G = 128), but at 4 no sampler CTA of the next
-  // group can co-reside, and co-running measured slower than back to back
-  // (step 9.88 ms at 4/SM vs 11.23 ms at 3/SM)
-  static const int env_ctas = [] {
-    const char* e = getenv("RG_GATHER_CTAS_PER_SM");
-    return e ? std::max(1, atoi(e)) : 4;
-  }();
-  static const int kernel = [] {  // 1: staged union (default), 0: window-major
-    const char* e = getenv("RG_GATHER_UNION");
-    return e ? atoi(e) : 1;
-  }();
   // staged rows per CTA <= ~56 KB: 4 CTAs per SM at Products (128 ids x 400 B)
   static const int kw_max = [] {
     const char* e = getenv("RG_GATHER_KW");
@@ -772,7 +617,9 @@ extern "C" int rg_gather_window(const uint32_t* d_bm, const int32_t* d_wpre, int
   int kw = kw_max;
   while (kw > 1 && (int64_t)32 * kw * nvec * 16 > 56 * 1024) kw >>= 1;
   const size_t srows = (size_t)32 * kw * nvec * 16;
-  if (kernel && srows <= 200 * 1024) {
+  RG_REQUIRE(srows <= 200 * 1024, "rg_gather_window: rows of %d floats too wide to stage",
+             stride);
+  {
     cudaStream_t st = (cudaStream_t)stream;
     auto go = [&](auto kern) {
       static bool attr = false;  // per instantiation
@@ -796,10 +643,6 @@ extern "C" int rg_gather_window(const uint32_t* d_bm, const int32_t* d_wpre, int
     if (kw == 2) return go(gather_staged_kernel<2>);
     return go(gather_staged_kernel<1>);
   }
-  gather_window_kernel<<<kNumSMs * env_ctas, kGatherWarps * 32, 0, (cudaStream_t)stream>>>(
-      d_bm, d_wpre, nwords, G, cap, d_route, bases, src_stride, stride, nvec, dq, dr, my_part,
-      peer_mask, d_out, d_counters, q);
-  return check_launch("gather_window");
 }
 
 extern "C" int rg_route_with_cache(const uint32_t* d_base_route, int64_t n, const int32_t* d_hot,
