@@ -410,7 +410,7 @@ class WorkerPipeline:
         # row (Products G = 128: 56, measured ~35 -> 5.97 vs 6.70 ms); for
         # sparse groups (papers100M-shaped, G = 8: 0.31) the id-list queue
         # gather is faster (15.8 vs ~3.5 ms per launch)
-        dense = ng * self.cap_in >= 4 * self.dg.n
+        dense = ng * self.cap_in >= 4 * self.dg.n and st.stride * 4 * 32 <= 200 * 1024
         if self.gather_mode == "window" and dense and ng <= 128 and peer_mask == 0:
             # staged union gather straight from the group's input bitmaps
             self.gather_kernel = "gather_staged_kernel (rg_gather_window)"
