@@ -74,6 +74,22 @@ def block_from_slot(smp, slot: int, nfront: np.ndarray) -> DeviceBlock:
     return DeviceBlock(fr, ell, cnt, list(smp.step_fan), smp.dg.n)
 
 
+def wgrad(a: torch.Tensor, dz: torch.Tensor) -> torch.Tensor:
+    """a.T @ dz for tall operands (the weight gradient over a level's rows,
+    model.py:130-131).  cuBLAS runs a [d_in x K] @ [K x d_out] product with a
+    tiny output on a couple of CTAs; with K in the tens of thousands the rows
+    are split into chunks multiplied as one batched GEMM and summed (a
+    different fp32 summation order than one GEMM: parity is rel 1e-5)."""
+    k = a.shape[0]
+    chunk = 4096
+    if k < 4 * chunk:
+        return a.T @ dz
+    n = k // chunk
+    head = torch.bmm(a[: n * chunk].view(n, chunk, -1).transpose(1, 2),
+                     dz[: n * chunk].view(n, chunk, -1)).sum(dim=0)
+    return head + a[n * chunk:].T @ dz[n * chunk:] if n * chunk < k else head
+
+
 def _forward(block: DeviceBlock, h: torch.Tensor, params: list[LayerParams]):
     """h: the bundle rows [|input|, >= feat_dim] (a row-strided view is fine)."""
     L = len(params)
@@ -114,7 +130,7 @@ def loss_and_grad(block: DeviceBlock, rows: torch.Tensor, labels: torch.Tensor,
         h, h_self, mean, z, pos = saved[l]
         if l < L - 1:
             dz = dz * (z > 0)
-        grads[l] = LayerParams(h_self.T @ dz, mean.T @ dz, dz.sum(dim=0))
+        grads[l] = LayerParams(wgrad(h_self, dz), wgrad(mean, dz), dz.sum(dim=0))
         if l > 0:
             d = L - 1 - l
             dself = dz @ p.w_self.T
@@ -184,7 +200,7 @@ class GraphTrainer:
             h_self, mean, z, pos, d = saved[l]
             if l < L - 1:
                 dz = dz * (z > 0)
-            gws, gwn, gb = h_self.T @ dz, mean.T @ dz, dz.sum(dim=0)
+            gws, gwn, gb = wgrad(h_self, dz), wgrad(mean, dz), dz.sum(dim=0)
             if l > 0:
                 dself = dz @ p.w_self.T
                 dmean = dz @ p.w_neigh.T
