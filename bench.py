@@ -908,11 +908,11 @@ def run_train_leg(dg, store, part, train, cfg, hot, labels_np, group: int, group
     loss_sum = torch.zeros((), dtype=torch.float64, device="cuda")
     trainer = model.GraphTrainer(params, labels, d, dg.n, 0.05) if graphs else None
 
-    def train_group(smp, rows_buf, ng, nf):
+    def train_group(smp, rows_buf, ng, nf, lock=None):
         nonlocal params
         if trainer is not None:
             for b in range(ng):
-                trainer.step(smp, rows_buf, b)
+                trainer.step(smp, rows_buf, b, lock)
             return
         for b in range(ng):
             blk = model.block_from_slot(smp, b, nf[:, b])
@@ -927,7 +927,8 @@ def run_train_leg(dg, store, part, train, cfg, hot, labels_np, group: int, group
             try:
                 while (item := prod.next_group()) is not None:
                     i0, ng, slot, nf = item
-                    train_group(pipe.samplers[slot], pipe.row_bufs[slot], ng, nf)
+                    train_group(pipe.samplers[slot], pipe.row_bufs[slot], ng, nf,
+                                prod.capture_lock)
                     prod.release(slot)
             finally:
                 prod.close()

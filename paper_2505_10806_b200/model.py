@@ -210,36 +210,46 @@ class GraphTrainer:
             p.bias.sub_(self.lr_t * gb)
         self.loss_sum.add_(loss.double())
 
-    def step(self, smp, rows_buf, b: int) -> None:
-        """One batch on the current stream (capturing its graph on first use)."""
+    def step(self, smp, rows_buf, b: int, capture_lock=None) -> None:
+        """One batch on the current stream (capturing its graph on first use;
+        capture_lock, e.g. GroupProducer.capture_lock, keeps another thread's
+        CUDA calls out of the capture)."""
         key = (smp.front[0].data_ptr(), rows_buf.data_ptr(), int(b))
         g = self.graphs.get(key)
         if g is None:
-            cur = torch.cuda.current_stream()
-            if not self.graphs:
-                # first capture: let cuBLAS / the allocator initialise outside it,
-                # on a side stream, on throw-away copies of the parameters
-                keep = [LayerParams(p.w_self.clone(), p.w_neigh.clone(), p.bias.clone())
-                        for p in self.params]
-                loss0 = self.loss_sum.clone()
-                side = torch.cuda.Stream()
-                side.wait_stream(cur)
-                with torch.cuda.stream(side):
-                    self._body(smp, rows_buf, b)
-                cur.wait_stream(side)
-                for p, k in zip(self.params, keep):
-                    p.w_self.copy_(k.w_self)
-                    p.w_neigh.copy_(k.w_neigh)
-                    p.bias.copy_(k.bias)
-                self.loss_sum.copy_(loss0)
-            g = torch.cuda.CUDAGraph()
-            # thread_local: the GroupProducer thread keeps sampling / gathering
-            # on its own streams while this thread captures
-            with torch.cuda.graph(g, pool=self.pool, capture_error_mode="thread_local"):
-                self._body(smp, rows_buf, b)
-            self.graphs[key] = g
-            self.captures += 1
+            if capture_lock is not None:
+                with capture_lock:
+                    self._capture(smp, rows_buf, b, key)
+            else:
+                self._capture(smp, rows_buf, b, key)
+            g = self.graphs[key]
         g.replay()
+
+    def _capture(self, smp, rows_buf, b: int, key) -> None:
+        cur = torch.cuda.current_stream()
+        if not self.graphs:
+            # first capture: let cuBLAS / the allocator initialise outside it,
+            # on a side stream, on throw-away copies of the parameters
+            keep = [LayerParams(p.w_self.clone(), p.w_neigh.clone(), p.bias.clone())
+                    for p in self.params]
+            loss0 = self.loss_sum.clone()
+            side = torch.cuda.Stream()
+            side.wait_stream(cur)
+            with torch.cuda.stream(side):
+                self._body(smp, rows_buf, b)
+            cur.wait_stream(side)
+            for p, k in zip(self.params, keep):
+                p.w_self.copy_(k.w_self)
+                p.w_neigh.copy_(k.w_neigh)
+                p.bias.copy_(k.bias)
+            self.loss_sum.copy_(loss0)
+        g = torch.cuda.CUDAGraph()
+        # thread_local + the caller's capture_lock: the GroupProducer thread
+        # keeps its GPU work in flight but makes no CUDA calls meanwhile
+        with torch.cuda.graph(g, pool=self.pool, capture_error_mode="thread_local"):
+            self._body(smp, rows_buf, b)
+        self.graphs[key] = g
+        self.captures += 1
 
 
 def sgd_step(params: list[LayerParams], grads: list[LayerParams], lr: float) -> list[LayerParams]:

@@ -456,6 +456,7 @@ class GroupProducer:
         self._q: queue.Queue = queue.Queue()
         self._tokens = threading.Semaphore(pipe.nbuf)
         self._stop = threading.Event()
+        self.capture_lock = threading.Lock()
         self._done = False
         pin = torch.cuda.is_available()
         self._nf = [torch.zeros((pipe.sampler.L + 1, pipe.G), dtype=I32).pin_memory()
@@ -478,14 +479,23 @@ class GroupProducer:
                         return
                 if self._stop.is_set():
                     return
-                ng = pipe.step_overlapped(i0)
-                slot = pipe.last_slot
-                with torch.cuda.stream(pipe.s_gather):
-                    self._nf[slot].copy_(pipe.samplers[slot].nfront, non_blocking=True)
-                    if self.latency_ms > 0:
-                        self._cnt[slot][:ng].copy_(pipe.counters[i0:i0 + ng], non_blocking=True)
-                    self._ev[slot].record(pipe.s_gather)
-                self._ev[slot].synchronize()
+                # CUDA API work of this thread is excluded while the consumer
+                # captures a CUDA graph (capture_lock): a concurrent launch or
+                # sync from another thread can invalidate a capture
+                with self.capture_lock:
+                    ng = pipe.step_overlapped(i0)
+                    slot = pipe.last_slot
+                    with torch.cuda.stream(pipe.s_gather):
+                        self._nf[slot].copy_(pipe.samplers[slot].nfront, non_blocking=True)
+                        if self.latency_ms > 0:
+                            self._cnt[slot][:ng].copy_(pipe.counters[i0:i0 + ng],
+                                                       non_blocking=True)
+                        self._ev[slot].record(pipe.s_gather)
+                while True:
+                    with self.capture_lock:
+                        if self._ev[slot].query():
+                            break
+                    time.sleep(50e-6)
                 if self.latency_ms > 0:
                     masks = self._cnt[slot][:ng, _lib.RG_CNT_OWNER_MASK].numpy().view(np.uint32)
                     rpcs = sum(bin(int(m)).count("1") for m in masks)

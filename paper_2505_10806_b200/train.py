@@ -234,11 +234,11 @@ def _run(cfg: RunConfig) -> list[WorkerResult]:
             if trainer is not None:
                 loss_sum = trainer.loss_sum.clone()
 
-            def train_group(smp, rows_buf, ng, nf):
+            def train_group(smp, rows_buf, ng, nf, lock=None):
                 nonlocal params
                 if trainer is not None:
                     for b in range(ng):
-                        trainer.step(smp, rows_buf, b)
+                        trainer.step(smp, rows_buf, b, lock)
                     return
                 for b in range(ng):
                     blk = model.block_from_slot(smp, b, nf[:, b])
@@ -260,7 +260,8 @@ def _run(cfg: RunConfig) -> list[WorkerResult]:
                         i0, ng, slot, nf = item
                         if not rapid and cfg.latency_ms > 0:
                             _sleep_rpcs(pipe, i0, ng, cfg.latency_ms)
-                        train_group(pipe.samplers[slot], pipe.row_bufs[slot], ng, nf)
+                        train_group(pipe.samplers[slot], pipe.row_bufs[slot], ng, nf,
+                                    prod.capture_lock)
                         prod.release(slot)
                 finally:
                     prod.close()
