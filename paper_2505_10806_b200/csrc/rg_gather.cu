@@ -292,19 +292,42 @@ __global__ void __launch_bounds__(kGatherWarps * 32, 4)
 #endif
 
 // ---- staged union gather: each source row read once per group -------------
-// The window kernel above still moves every bundle row through L2 twice (the
-// source read — an L2 hit for all but the first batch — and the write):
-// 68.8 GB of L2 traffic per G = 128 Products launch, near the full-chip L2
-// slice throughput, while the bundle writes alone (34.4 GB) need ~4.6 ms at
-// the measured write-only HBM rate (7.5 TB/s, tools/hbm_probe.py).  Here a
-// CTA owns a window of 32*kW ids for ALL G batches: phase 1 stages every
-// present source row of the window in shared memory (each row read from
-// HBM once per group); phase 2 writes, batch by batch, that batch's rows of
-// the window as one contiguous run (ranks wpre[b][w0] ..).  (A warp-per-id
-// scatter — each row stored straight to every batch holding it — reads once
-// too but scatters 400-B writes over all G bundles at once and measured
-// 11.7 ms: HBM write locality matters more than the reads.)
-template <int kW>
+// A gather that reads every batch's rows separately moves each bundle row
+// through L2 twice (the source read — an L2 hit for all but the first batch
+// — and the write): 68.8 GB of L2 traffic per G = 128 Products launch, while
+// the bundle writes alone (34.4 GB) need ~4.6 ms at the measured write-only
+// HBM rate (7.5 TB/s, tools/hbm_probe.py).  Here a CTA owns a window of
+// 32*kW ids for ALL G batches: phase 1 stages every present source row of
+// the window in shared memory (each row read from HBM once per group);
+// phase 2 writes, batch by batch, that batch's rows of the window as one
+// contiguous run (ranks wpre[b][w0] ..).  (A warp-per-id scatter — each row
+// stored straight to every batch holding it — reads once too but scatters
+// 400-B writes over all G bundles at once and measured 11.7 ms: HBM write
+// locality matters more than the reads.)
+// kBulk: phase 2 hands each run of consecutive present ids to the TMA engine
+// as one bulk shared->global copy (cp.async.bulk; rows are 16-B multiples),
+// issued by the lane that owns the run's first id, instead of moving 16-B
+// vectors through registers; the staging buffer is double-buffered so
+// window k+1 is loaded while the bulk copies of window k drain.
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"((uint32_t)__cvta_generic_to_shared(ssrc)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+template <int kW, bool kBulk>
 __global__ void __launch_bounds__(kGatherWarps * 32, RG_STAGED_MIN_CTAS)
     gather_staged_kernel(const uint32_t* __restrict__ bm, const int32_t* __restrict__ wpre,
                          int64_t nwords, int G, int64_t cap, const uint32_t* __restrict__ route,
@@ -329,8 +352,13 @@ __global__ void __launch_bounds__(kGatherWarps * 32, RG_STAGED_MIN_CTAS)
     (&s_cnt[0][0])[i] = 0;
   if (threadIdx.x < 16) s_base[threadIdx.x] = bases.p[threadIdx.x];
   const int64_t nwin = (nwords + kW - 1) / kW;
-  for (;;) {
+  const uint32_t row_bytes = (uint32_t)nvec * 16u;
+  for (unsigned it = 0;; ++it) {
+    // kBulk: the bulk copies that read this window's staging buffer (issued
+    // two windows ago) have finished reading it
+    if constexpr (kBulk) bulk_wait_read1();
     __syncthreads();  // previous window fully written out; counters zeroed
+    float4* rows = s_rows + (kBulk ? (it & 1u) * (unsigned)(kIds * nvec) : 0u);
     if (threadIdx.x == 0) s_win = atomicAdd(queue, 1u);
     if (threadIdx.x < kW) s_present[threadIdx.x] = 0;
     if (threadIdx.x < 16 * kW) (&s_mq[0][0])[threadIdx.x] = 0;
@@ -395,10 +423,11 @@ __global__ void __launch_bounds__(kGatherWarps * 32, RG_STAGED_MIN_CTAS)
             v[u] = sp[u] ? ld_stream(reinterpret_cast<const float4*>(sp[u]) + c)
                          : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-          for (int u = 0; u < kR; ++u) s_rows[(r0 + u) * nvec + c] = v[u];
+          for (int u = 0; u < kR; ++u) rows[(r0 + u) * nvec + c] = v[u];
         }
       }
     }
+    if constexpr (kBulk) fence_proxy_async_smem();  // staged rows -> the TMA's view
     __syncthreads();
     // phase 2a: provenance of the window for this warp's batches, one batch
     // per lane (batch w + 8l belongs to lane l of warp w in every window, so
@@ -431,6 +460,43 @@ __global__ void __launch_bounds__(kGatherWarps * 32, RG_STAGED_MIN_CTAS)
       }
     }
     // phase 2b: each batch's run of the window, contiguous
+    if constexpr (kBulk) {
+      // lane l owns id 32q + l.  Consecutive ids of the batch are
+      // consecutive rows both in the staging buffer and in the batch's run,
+      // so each maximal run of set bits (across word boundaries) is one bulk
+      // copy, issued by the lane of its first id; its output rank is the
+      // popcount of the batch's bits below it.
+      for (int bb = warp; bb < G; bb += kGatherWarps) {
+        uint32_t wd[kW];
+#pragma unroll
+        for (int q = 0; q < kW; ++q) wd[q] = s_words[bb * kW + q];
+        int r = s_rbase[bb];
+        float* dstb = out + (int64_t)bb * cap * stride;
+#pragma unroll
+        for (int q = 0; q < kW; ++q) {
+          const uint32_t word = wd[q];
+          const bool prev = lane ? (word >> (lane - 1)) & 1u : (q ? wd[q - 1] >> 31 : 0u);
+          if (((word >> lane) & 1u) && !prev) {
+            // trailing ones from this id on, continued into the next words
+            int len = __clz(__brev(~(word >> lane)));
+            bool open = len == 32 - lane;
+#pragma unroll
+            for (int q2 = q + 1; q2 < kW; ++q2) {
+              if (open) {
+                const int t = __clz(__brev(~wd[q2]));
+                len += t;
+                open = t == 32;
+              }
+            }
+            bulk_s2g(dstb + (int64_t)(r + __popc(word & lt)) * stride, rows + (q * 32 + lane) * nvec,
+                     row_bytes * (uint32_t)len);
+          }
+          r += __popc(word);
+        }
+      }
+      bulk_commit();
+      continue;
+    }
     for (int bb = warp; bb < G; bb += kGatherWarps) {
       const uint32_t wd = lane < kW ? s_words[bb * kW + lane] : 0u;
       if (__reduce_or_sync(kFull, wd) == 0u) continue;
@@ -453,7 +519,7 @@ __global__ void __launch_bounds__(kGatherWarps * 32, RG_STAGED_MIN_CTAS)
             float4 v[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-              if (j[u] >= 0) v[u] = s_rows[j[u] * nvec + c];
+              if (j[u] >= 0) v[u] = rows[j[u] * nvec + c];
 #pragma unroll
             for (int u = 0; u < 4; ++u)
               if (j[u] >= 0) st_stream(dst + (int64_t)(k + u) * nvec + c, v[u]);
@@ -463,6 +529,7 @@ __global__ void __launch_bounds__(kGatherWarps * 32, RG_STAGED_MIN_CTAS)
       }
     }
   }
+  if constexpr (kBulk) bulk_wait_all();  // the staging buffers outlive every copy
   __syncthreads();
   for (int i = threadIdx.x; i < G * RG_NCOUNTERS; i += blockDim.x) {
     const int bb = i / RG_NCOUNTERS, k = i - bb * RG_NCOUNTERS;
@@ -609,39 +676,82 @@ extern "C" int rg_gather_window(const uint32_t* d_bm, const int32_t* d_wpre, int
   const int dq = 32 / nvec, dr = 32 % nvec;
   unsigned* q = queue_slot((cudaStream_t)stream);
   if (!q) return check_launch("gather window queue");
-  // staged rows per CTA <= ~56 KB: 4 CTAs per SM at Products (128 ids x 400 B)
-  static const int kw_max = [] {
-    const char* e = getenv("RG_GATHER_KW");
-    return e ? std::max(1, std::min(4, atoi(e))) : 2;  // 2: 5.96 ms, 4: 5.97, 1: 6.79
+  // Phase 2 by TMA bulk copies (default) or through registers
+  // (RG_GATHER_BULK=0).  Products G = 128, ms per launch: bulk 128-id windows
+  // 5.87, 64-id 5.99; registers 64-id 6.04, 128-id 5.97.  With the row
+  // reads removed (diagnostic build) the bulk kernel still needs 5.41 ms:
+  // the bundle write pattern (~6.4 TB/s here), not instruction issue (bulk
+  // executes 3x fewer instructions than the register copy), bounds it.
+  static const int bulk_env = [] {
+    const char* e = getenv("RG_GATHER_BULK");
+    return e ? atoi(e) : -1;  // -1: by size
   }();
-  int kw = kw_max;
-  while (kw > 1 && (int64_t)32 * kw * nvec * 16 > 56 * 1024) kw >>= 1;
-  const size_t srows = (size_t)32 * kw * nvec * 16;
-  RG_REQUIRE(srows <= 200 * 1024, "rg_gather_window: rows of %d floats too wide to stage",
+  static const int kw_env = [] {
+    const char* e = getenv("RG_GATHER_KW");  // ids per window / 32
+    return e ? std::max(1, std::min(4, atoi(e))) : 0;
+  }();
+  // staged rows per window <= ~56 KB
+  auto window_words = [&](int kw) {
+    while (kw > 1 && (int64_t)32 * kw * nvec * 16 > 56 * 1024) kw >>= 1;
+    return kw;
+  };
+  int kw = window_words(kw_env ? kw_env : 4);
+  // bulk needs the staging buffer twice and enough windows per CTA for the
+  // double buffer to pay (BASELINE config 0, ~6 windows per CTA: registers
+  // 0.129 vs bulk 0.137 ms)
+  bool bulk = bulk_env != 0 && 2 * (size_t)32 * kw * nvec * 16 <= 200 * 1024 &&
+              (bulk_env == 1 || (nwords + kw - 1) / kw >= (int64_t)16 * kNumSMs);
+  if (!bulk) kw = window_words(kw_env ? kw_env : 2);
+  const size_t sbuf = (size_t)32 * kw * nvec * 16;  // one window's staged rows
+  RG_REQUIRE(sbuf <= 200 * 1024, "rg_gather_window: rows of %d floats too wide to stage",
              stride);
+  const size_t srows = bulk ? 2 * sbuf : sbuf;
   {
     cudaStream_t st = (cudaStream_t)stream;
     auto go = [&](auto kern) {
-      static bool attr = false;  // per instantiation
-      if (!attr) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr = true;
-      }
-      int per_sm = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kGatherWarps * 32, srows);
+      // every call: the attribute is per kernel and per device, and all the
+      // instantiations share this lambda's type (a static flag here would
+      // only ever cover the first one)
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) !=
+          cudaSuccess)
+        return check_launch("gather_staged attribute");
       static const int cap_sm = [] {
         const char* e = getenv("RG_GATHER_STAGED_CTAS");
         return e ? std::max(1, atoi(e)) : 0;
       }();
+      size_t dyn = srows;
+      if (bulk) {
+        // the TMA engine drains the stores, so 2 CTAs per SM carry the
+        // launch; the rest of the SM's shared memory is reserved too, so no
+        // other kernel (the next group's sampler on the other stream) lands
+        // beside it: a co-resident sampler stretches the gather's
+        // latency-bound staging phase (Products: 12.96 vs 9.26 ms per step)
+        const int want_sm = cap_sm ? cap_sm : 2;
+        int dev = 0, smem_sm = 0, reserved = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+        cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, kern);
+        const int64_t fill = (int64_t)smem_sm / want_sm - reserved - (int64_t)fa.sharedSizeBytes;
+        dyn = (size_t)std::max<int64_t>((int64_t)srows, std::min<int64_t>(fill, 200 * 1024));
+      }
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kGatherWarps * 32, dyn);
       if (cap_sm) per_sm = std::min(per_sm, cap_sm);
-      kern<<<kNumSMs * std::max(1, per_sm), kGatherWarps * 32, srows, st>>>(
+      kern<<<kNumSMs * std::max(1, per_sm), kGatherWarps * 32, dyn, st>>>(
           d_bm, d_wpre, nwords, G, cap, d_route, bases, src_stride, stride, nvec, dq, dr, my_part,
           peer_mask, d_out, d_counters, q);
       return check_launch("gather_staged");
     };
-    if (kw == 4) return go(gather_staged_kernel<4>);
-    if (kw == 2) return go(gather_staged_kernel<2>);
-    return go(gather_staged_kernel<1>);
+    if (bulk) {
+      if (kw == 4) return go(gather_staged_kernel<4, true>);
+      if (kw == 2) return go(gather_staged_kernel<2, true>);
+      return go(gather_staged_kernel<1, true>);
+    }
+    if (kw == 4) return go(gather_staged_kernel<4, false>);
+    if (kw == 2) return go(gather_staged_kernel<2, false>);
+    return go(gather_staged_kernel<1, false>);
   }
 }
 
