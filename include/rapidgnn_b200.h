@@ -272,6 +272,24 @@ int rg_sage_mean_bwd(int32_t dtype, const void* d_dself, const void* d_dmean, in
                      const int32_t* d_n_src, const int32_t* d_n_dst, int32_t* d_self_of,
                      void* d_dh, void* stream);
 
+/* ---- training-step head and update (model.py:107-146) ---------------
+ * rg_softmax_xent: for the live rows r < min(*d_n, cap) of logits [cap, C]
+ * (C <= 64, dtype as above): y = labels[front0[r]], nll_r = log(sum_j
+ * exp(l_rj - m_r)) - (l_ry - m_r), d_dz[r, j] = (softmax_rj - [j == y]) / n;
+ * padding rows get zero gradient; *d_loss_acc += (sum_r nll_r) / n as a
+ * double.  One CTA, fixed summation order (deterministic).
+ * Replaces the mean softmax cross-entropy and its gradient of
+ * loss_and_grad (model.py:107-124).                                      */
+int rg_softmax_xent(int32_t dtype, const void* d_logits, int32_t C, int64_t cap,
+                    const int32_t* d_n, const int64_t* d_labels, const int32_t* d_front0,
+                    void* d_dz, double* d_loss_acc, void* stream);
+/* rg_sgd_apply: for t < n_tensors (<= 3): w_t[i] -= lr * sum_{c < chunks_t}
+ * g_t[c * n_t + i] (chunk partials summed in chunk order, then the
+ * reference's rounding: lr * g rounded, then subtracted).  sgd_step,
+ * model.py:139-146.                                                       */
+int rg_sgd_apply(int32_t dtype, int32_t n_tensors, void* const* h_w, const void* const* h_g,
+                 const int64_t* h_n, const int32_t* h_chunks, double lr, void* stream);
+
 /* ---- host-side graph materialisation (graph.py, partition.py) ------- */
 int rg_philox_raw(uint64_t key0, uint64_t key1, int64_t count, uint64_t* h_out);
 /* CSR of gnnpipe.graph.synth_powerlaw(n, m, ., ., seed) with the Philox

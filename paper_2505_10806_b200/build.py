@@ -20,7 +20,7 @@ LIB = HERE / "librapidgnn_b200.so"
 STAMP = HERE / ".build_stamp"
 
 CU_SOURCES = ["rg_abi.cu", "rg_sampler.cu", "rg_gather.cu", "rg_prefetch.cu",
-              "rg_plan.cu", "rg_sage.cu"]
+              "rg_plan.cu", "rg_sage.cu", "rg_train.cu"]
 CPP_SOURCES = ["rg_host.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",

@@ -11,11 +11,14 @@ reference to ~1e-6 relative, not bit-for-bit.
 
 from __future__ import annotations
 
+import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
 import torch
 
+from . import _lib
 from .aggregate import sage_mean, sage_mean_backward, sage_positions
 
 
@@ -74,20 +77,40 @@ def block_from_slot(smp, slot: int, nfront: np.ndarray) -> DeviceBlock:
     return DeviceBlock(fr, ell, cnt, list(smp.step_fan), smp.dg.n)
 
 
+_WGRAD_CHUNK = int(os.environ.get("RG_WGRAD_CHUNK", "256"))
+
+
 def wgrad(a: torch.Tensor, dz: torch.Tensor) -> torch.Tensor:
     """a.T @ dz for tall operands (the weight gradient over a level's rows,
     model.py:130-131).  cuBLAS runs a [d_in x K] @ [K x d_out] product with a
-    tiny output on a couple of CTAs; with K in the tens of thousands the rows
-    are split into chunks multiplied as one batched GEMM and summed (a
-    different fp32 summation order than one GEMM: parity is rel 1e-5)."""
+    tiny output on a couple of CTAs; with K in the thousands the rows are
+    split into 256-row chunks multiplied as one batched GEMM (hundreds of
+    CTAs) and summed (a different fp32 summation order than one GEMM: parity
+    is rel 1e-5).  Products training step, GPU ms per batch: chunk 4096
+    0.82, 1024 0.64, 512 0.61, 256 0.59 (tools/train_probe.py)."""
     k = a.shape[0]
-    chunk = 4096
+    chunk = _WGRAD_CHUNK
     if k < 4 * chunk:
         return a.T @ dz
     n = k // chunk
     head = torch.bmm(a[: n * chunk].view(n, chunk, -1).transpose(1, 2),
                      dz[: n * chunk].view(n, chunk, -1)).sum(dim=0)
     return head + a[n * chunk:].T @ dz[n * chunk:] if n * chunk < k else head
+
+
+def wgrad_parts(a: torch.Tensor, dz: torch.Tensor) -> torch.Tensor:
+    """wgrad's chunk partials, unsummed: [chunks, d_in, d_out] (the sum runs
+    inside rg_sgd_apply, in chunk order)."""
+    k = a.shape[0]
+    chunk = _WGRAD_CHUNK
+    if k < 4 * chunk:
+        return (a.T @ dz)[None]
+    n = k // chunk
+    head = torch.bmm(a[: n * chunk].view(n, chunk, -1).transpose(1, 2),
+                     dz[: n * chunk].view(n, chunk, -1))
+    if n * chunk < k:
+        head = torch.cat([head, (a[n * chunk:].T @ dz[n * chunk:])[None]])
+    return head
 
 
 def _forward(block: DeviceBlock, h: torch.Tensor, params: list[LayerParams]):
@@ -156,10 +179,11 @@ class GraphTrainer:
         self.params = [LayerParams(p.w_self.clone(), p.w_neigh.clone(), p.bias.clone())
                        for p in params]
         self.dtype = self.params[0].w_self.dtype
-        self.labels = labels
+        self.dcode = {torch.float32: 0, torch.float64: 1}[self.dtype]
+        self.labels = labels.long().contiguous()
+        self.lr = float(lr)
         self.feat_dim = int(feat_dim)
         self.n = int(num_nodes)
-        self.lr_t = torch.tensor(lr, dtype=self.dtype, device=labels.device)
         self.loss_sum = torch.zeros((), dtype=torch.float64, device=labels.device)
         self.rank = torch.empty(self.n, dtype=torch.int32, device=labels.device)
         self.pool = torch.cuda.graph_pool_handle()
@@ -177,38 +201,41 @@ class GraphTrainer:
         saved = []
         for l, p in enumerate(params):
             d = L - 1 - l
-            pos = sage_positions(front[d + 1], front[d], smp.ell[d][b], smp.cnt[d][b],
+            cnt = smp.cnt[d][b]
+            pos = sage_positions(front[d + 1], front[d], smp.ell[d][b], cnt,
                                  smp.step_fan[d], self.n, self.rank, dn[d + 1], dn[d])
-            mean, h_self = sage_mean(h, pos, smp.cnt[d][b], H=p.w_self.shape[0])
+            mean, h_self = sage_mean(h, pos, cnt, H=p.w_self.shape[0])
             z = h_self @ p.w_self + mean @ p.w_neigh + p.bias
-            saved.append((h_self, mean, z, pos, d))
+            saved.append((h_self, mean, z, pos, d, cnt))
             h = torch.clamp_min(z, 0) if l < L - 1 else z
+        # softmax cross-entropy over the live seeds and its gradient, one
+        # kernel (model.py:107-124); the loss accumulates into loss_sum
         cap0 = front[0].numel()
-        n0 = nf[0, b].to(self.dtype)
-        live = torch.arange(cap0, device=h.device) < nf[0, b]
-        y = self.labels[torch.where(live, front[0], 0).long()]
-        shifted = h - h.max(dim=1, keepdim=True).values
-        ex = torch.exp(shifted)
-        se = ex.sum(dim=1)
-        nll = -(shifted.gather(1, y[:, None])[:, 0] - torch.log(se))
-        loss = torch.where(live, nll, 0).sum() / n0
-        dz = ex / se[:, None]
-        dz.scatter_add_(1, y[:, None], -torch.ones((cap0, 1), dtype=dz.dtype, device=dz.device))
-        dz = torch.where(live[:, None], dz / n0, 0)
+        h = h.contiguous()
+        dz = torch.empty_like(h)
+        s = _lib.stream_handle()
+        _lib.call("rg_softmax_xent", self.dcode, h.data_ptr(), h.shape[1], cap0, dn[0],
+                  self.labels.data_ptr(), front[0].data_ptr(), dz.data_ptr(),
+                  self.loss_sum.data_ptr(), s)
         for l in range(L - 1, -1, -1):
             p = params[l]
-            h_self, mean, z, pos, d = saved[l]
+            h_self, mean, z, pos, d, cnt = saved[l]
             if l < L - 1:
                 dz = dz * (z > 0)
-            gws, gwn, gb = wgrad(h_self, dz), wgrad(mean, dz), dz.sum(dim=0)
+            gws, gwn, gb = wgrad_parts(h_self, dz), wgrad_parts(mean, dz), dz.sum(dim=0)
             if l > 0:
                 dself = dz @ p.w_self.T
                 dmean = dz @ p.w_neigh.T
-                dz = sage_mean_backward(dself, dmean, smp.cnt[d][b], pos)
-            p.w_self.sub_(self.lr_t * gws)
-            p.w_neigh.sub_(self.lr_t * gwn)
-            p.bias.sub_(self.lr_t * gb)
-        self.loss_sum.add_(loss.double())
+                dz = sage_mean_backward(dself, dmean, cnt, pos)
+            # SGD on the three tensors in one launch, the weight gradients'
+            # chunk partials summed inside (sgd_step, model.py:139-146)
+            ws = (p.w_self, p.w_neigh, p.bias)
+            gs = (gws, gwn, gb)
+            _lib.call("rg_sgd_apply", self.dcode, 3,
+                      (ctypes.c_void_p * 3)(*[w.data_ptr() for w in ws]),
+                      (ctypes.c_void_p * 3)(*[g.data_ptr() for g in gs]),
+                      (ctypes.c_int64 * 3)(*[w.numel() for w in ws]),
+                      (ctypes.c_int32 * 3)(gws.shape[0], gwn.shape[0], 1), self.lr, s)
 
     def step(self, smp, rows_buf, b: int, capture_lock=None) -> None:
         """One batch on the current stream (capturing its graph on first use;

@@ -473,6 +473,61 @@ def test_sage_mean_strided_rows(rg):
     assert np.array_equal(hself.cpu().numpy(), want_self)
 
 
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_softmax_xent_and_sgd_apply(rg, dtype):
+    """The training step's fused head and update (rg_softmax_xent,
+    rg_sgd_apply) against the reference's expressions (model.py:107-124,
+    139-146) in numpy: loss and gradient over the live seed rows (padding
+    rows zero), and w - lr * g with the chunk partials summed in order
+    (bit-exact: the same per-operation rounding)."""
+    import ctypes
+
+    from paper_2505_10806_b200 import _lib
+
+    rng = np.random.default_rng(5)
+    cap, n, C, nodes = 96, 77, 47, 500
+    logits = (rng.standard_normal((cap, C)) * 3).astype(dtype)
+    labels = rng.integers(0, C, nodes).astype(np.int64)
+    front0 = np.sort(rng.choice(nodes, cap, replace=False)).astype(np.int32)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    d_l, d_lab, d_f = dev(logits), dev(labels), dev(front0)
+    d_n = dev(np.array([n], np.int32))
+    d_dz = torch.full((cap, C), 7.0, dtype=d_l.dtype, device="cuda")
+    loss = torch.zeros((), dtype=torch.float64, device="cuda")
+    code = 0 if dtype == np.float32 else 1
+    _lib.call("rg_softmax_xent", code, d_l.data_ptr(), C, cap, d_n.data_ptr(), d_lab.data_ptr(),
+              d_f.data_ptr(), d_dz.data_ptr(), loss.data_ptr(), _lib.stream_handle())
+    x = logits[:n].astype(np.float64)
+    y = labels[front0[:n]]
+    sh = x - x.max(axis=1, keepdims=True)
+    se = np.exp(sh).sum(axis=1)
+    want_loss = float(np.mean(np.log(se) - sh[np.arange(n), y]))
+    want_dz = np.exp(sh) / se[:, None]
+    want_dz[np.arange(n), y] -= 1
+    want_dz /= n
+    tol = 2e-6 if dtype == np.float32 else 1e-12
+    got = d_dz.cpu().numpy()
+    assert np.all(got[n:] == 0)
+    assert np.allclose(got[:n], want_dz, rtol=tol * 10, atol=tol)
+    assert float(loss.item()) == pytest.approx(want_loss, rel=tol * 10)
+    # update: three tensors, 5 / 3 / 1 chunk partials
+    lr = 0.05
+    shapes = [(100, 32), (32, 47), (47,)]
+    chunks = [5, 3, 1]
+    ws = [rng.standard_normal(sh).astype(dtype) for sh in shapes]
+    gs = [rng.standard_normal((c,) + sh).astype(dtype) for c, sh in zip(chunks, shapes)]
+    d_ws, d_gs = [dev(w) for w in ws], [dev(g) for g in gs]
+    _lib.call("rg_sgd_apply", code, 3, (ctypes.c_void_p * 3)(*[w.data_ptr() for w in d_ws]),
+              (ctypes.c_void_p * 3)(*[g.data_ptr() for g in d_gs]),
+              (ctypes.c_int64 * 3)(*[w.size for w in ws]), (ctypes.c_int32 * 3)(*chunks), lr,
+              _lib.stream_handle())
+    for w, g, d_w in zip(ws, gs, d_ws):
+        s_ = g[0].copy()
+        for c in range(1, g.shape[0]):
+            s_ = s_ + g[c]
+        assert np.array_equal(d_w.cpu().numpy(), w - dtype(lr) * s_)
+
+
 @pytest.mark.parametrize("kind", ["pcg32", "sfc64", "xoshiro256pp"])
 def test_prng_variant_blocks_match_oracle(rg, small, kind):
     """Device PRNG-variant sampling == the variant oracle (fast and CTA paths)."""
