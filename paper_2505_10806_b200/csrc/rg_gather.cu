@@ -719,8 +719,12 @@ extern "C" int rg_gather_window(const uint32_t* d_bm, const int32_t* d_wpre, int
         const char* e = getenv("RG_GATHER_STAGED_CTAS");
         return e ? std::max(1, atoi(e)) : 0;
       }();
+      static const bool reserve = [] {
+        const char* e = getenv("RG_GATHER_RESERVE");
+        return e ? atoi(e) != 0 : true;
+      }();
       size_t dyn = srows;
-      if (bulk) {
+      if (bulk && reserve) {
         // the TMA engine drains the stores, so 2 CTAs per SM carry the
         // launch; the rest of the SM's shared memory is reserved too, so no
         // other kernel (the next group's sampler on the other stream) lands
