@@ -276,17 +276,19 @@ int rg_sage_mean_bwd(int32_t dtype, const void* d_dself, const void* d_dmean, in
  * rg_softmax_xent: for the live rows r < min(*d_n, cap) of logits [cap, C]
  * (C <= 64, dtype as above): y = labels[front0[r]], nll_r = log(sum_j
  * exp(l_rj - m_r)) - (l_ry - m_r), d_dz[r, j] = (softmax_rj - [j == y]) / n;
- * padding rows get zero gradient; *d_loss_acc += (sum_r nll_r) / n as a
- * double.  One CTA, fixed summation order (deterministic).
+ * padding rows get zero gradient; d_nll: cap-element scratch of the same
+ * dtype (receives nll_r); *d_loss_acc += (sum_r nll_r) / n as a double,
+ * summed in a fixed order (deterministic).
  * Replaces the mean softmax cross-entropy and its gradient of
  * loss_and_grad (model.py:107-124).                                      */
 int rg_softmax_xent(int32_t dtype, const void* d_logits, int32_t C, int64_t cap,
                     const int32_t* d_n, const int64_t* d_labels, const int32_t* d_front0,
-                    void* d_dz, double* d_loss_acc, void* stream);
+                    void* d_dz, void* d_nll, double* d_loss_acc, void* stream);
 /* rg_sgd_apply: for t < n_tensors (<= 3): w_t[i] -= lr * sum_{c < chunks_t}
- * g_t[c * n_t + i] (chunk partials summed in chunk order, then the
- * reference's rounding: lr * g rounded, then subtracted).  sgd_step,
- * model.py:139-146.                                                       */
+ * g_t[c * n_t + i].  The chunk partials are summed in a fixed order: S_k =
+ * in-order sum over c = k, k + 8, ... (k < 8), then ((S0 + S1) + (S2 + S3))
+ * + ((S4 + S5) + (S6 + S7)); then the reference's rounding: lr * g rounded,
+ * then subtracted.  sgd_step, model.py:139-146.                           */
 int rg_sgd_apply(int32_t dtype, int32_t n_tensors, void* const* h_w, const void* const* h_g,
                  const int64_t* h_n, const int32_t* h_chunks, double lr, void* stream);
 

@@ -213,9 +213,10 @@ class GraphTrainer:
         cap0 = front[0].numel()
         h = h.contiguous()
         dz = torch.empty_like(h)
+        nll = torch.empty(cap0, dtype=h.dtype, device=h.device)
         s = _lib.stream_handle()
         _lib.call("rg_softmax_xent", self.dcode, h.data_ptr(), h.shape[1], cap0, dn[0],
-                  self.labels.data_ptr(), front[0].data_ptr(), dz.data_ptr(),
+                  self.labels.data_ptr(), front[0].data_ptr(), dz.data_ptr(), nll.data_ptr(),
                   self.loss_sum.data_ptr(), s)
         for l in range(L - 1, -1, -1):
             p = params[l]

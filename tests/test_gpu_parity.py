@@ -495,8 +495,10 @@ def test_softmax_xent_and_sgd_apply(rg, dtype):
     d_dz = torch.full((cap, C), 7.0, dtype=d_l.dtype, device="cuda")
     loss = torch.zeros((), dtype=torch.float64, device="cuda")
     code = 0 if dtype == np.float32 else 1
+    nll = torch.empty(cap, dtype=d_l.dtype, device="cuda")
     _lib.call("rg_softmax_xent", code, d_l.data_ptr(), C, cap, d_n.data_ptr(), d_lab.data_ptr(),
-              d_f.data_ptr(), d_dz.data_ptr(), loss.data_ptr(), _lib.stream_handle())
+              d_f.data_ptr(), d_dz.data_ptr(), nll.data_ptr(), loss.data_ptr(),
+              _lib.stream_handle())
     x = logits[:n].astype(np.float64)
     y = labels[front0[:n]]
     sh = x - x.max(axis=1, keepdims=True)
@@ -510,10 +512,10 @@ def test_softmax_xent_and_sgd_apply(rg, dtype):
     assert np.all(got[n:] == 0)
     assert np.allclose(got[:n], want_dz, rtol=tol * 10, atol=tol)
     assert float(loss.item()) == pytest.approx(want_loss, rel=tol * 10)
-    # update: three tensors, 5 / 3 / 1 chunk partials
+    # update: three tensors, 21 / 3 / 1 chunk partials
     lr = 0.05
     shapes = [(100, 32), (32, 47), (47,)]
-    chunks = [5, 3, 1]
+    chunks = [21, 3, 1]
     ws = [rng.standard_normal(sh).astype(dtype) for sh in shapes]
     gs = [rng.standard_normal((c,) + sh).astype(dtype) for c, sh in zip(chunks, shapes)]
     d_ws, d_gs = [dev(w) for w in ws], [dev(g) for g in gs]
@@ -522,9 +524,13 @@ def test_softmax_xent_and_sgd_apply(rg, dtype):
               (ctypes.c_int64 * 3)(*[w.size for w in ws]), (ctypes.c_int32 * 3)(*chunks), lr,
               _lib.stream_handle())
     for w, g, d_w in zip(ws, gs, d_ws):
-        s_ = g[0].copy()
-        for c in range(1, g.shape[0]):
-            s_ = s_ + g[c]
+        part = []
+        for k in range(8):  # in-order sums over c = k, k + 8, ...
+            acc = np.zeros_like(g[0])
+            for c in range(k, g.shape[0], 8):
+                acc = g[c].copy() if c == k else acc + g[c]
+            part.append(acc)
+        s_ = ((part[0] + part[1]) + (part[2] + part[3])) + ((part[4] + part[5]) + (part[6] + part[7]))
         assert np.array_equal(d_w.cpu().numpy(), w - dtype(lr) * s_)
 
 
