@@ -205,7 +205,10 @@ class GraphTrainer:
             pos = sage_positions(front[d + 1], front[d], smp.ell[d][b], cnt,
                                  smp.step_fan[d], self.n, self.rank, dn[d + 1], dn[d])
             mean, h_self = sage_mean(h, pos, cnt, H=p.w_self.shape[0])
-            z = h_self @ p.w_self + mean @ p.w_neigh + p.bias
+            # bias + h_self @ Ws + mean @ Wn as two accumulating GEMMs (no
+            # separate add launches)
+            z = torch.addmm(p.bias, h_self, p.w_self)
+            z.addmm_(mean, p.w_neigh)
             saved.append((h_self, mean, z, pos, d, cnt))
             h = torch.clamp_min(z, 0) if l < L - 1 else z
         # softmax cross-entropy over the live seeds and its gradient, one
@@ -222,7 +225,7 @@ class GraphTrainer:
             p = params[l]
             h_self, mean, z, pos, d, cnt = saved[l]
             if l < L - 1:
-                dz = dz * (z > 0)
+                dz = torch.ops.aten.threshold_backward(dz, z, 0)  # dz * (z > 0)
             gws, gwn, gb = wgrad_parts(h_self, dz), wgrad_parts(mean, dz), dz.sum(dim=0)
             if l > 0:
                 dself = dz @ p.w_self.T
