@@ -36,7 +36,6 @@ constexpr int kQueueBatches = 128;        // largest group G of one rg_sample_le
 // 24 12,148; 32 11,924; the earlier per-item warp decode at 8: 12,054;
 // another box: 10 12,796; 12 12,716; 14 12,698)
 constexpr unsigned kClaim = 10;
-constexpr unsigned kHubItems = 2048;      // leading items claimed singly (see the claim loop)
 
 __device__ __forceinline__ void mark(uint32_t* bm, int32_t v) {
   atomicOr(bm + (v >> 5), 1u << (v & 31));
@@ -337,7 +336,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32)
                         const uint64_t* __restrict__ rng_seed, int32_t* __restrict__ ell,
                         int32_t* __restrict__ cnt, uint32_t* __restrict__ bm, int64_t nwords,
                         int32_t* __restrict__ slow, int sorted_rows, int prng,
-                        unsigned* __restrict__ queue, unsigned claim, unsigned hub_cap) {
+                        unsigned* __restrict__ queue, unsigned claim) {
   __shared__ uint64_t s_key[kSampleWarps][64];
   __shared__ int32_t s_pos[kSampleWarps][96];
   __shared__ uint64_t s_seed[kQueueBatches];  // step seed s_d of every batch
@@ -363,6 +362,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32)
   // one launch-wide queue of items k = j*G + b (frontier rank j of batch b):
   // rank-major, so the low (hub-heavy) ranks of every batch go first and the
   // light tail balances across all SMs; warps claim kClaim items at a time
+  // (strided, below)
   const unsigned items = s_items * (unsigned)G;
   // batches past the shared-memory tables (G > kQueueBatches: API callers
   // sampling thousands of seeds sets at once) read / derive theirs
@@ -429,40 +429,29 @@ __global__ void __launch_bounds__(kSampleWarps * 32)
         mark(bmb, nb);
       }
   };
-  // The lowest ranks hold the hubs (frontiers are id-sorted and the
-  // generator's hubs have low ids), whose key streaming is serial per warp:
-  // the first kHubItems items are claimed one at a time from their own
-  // counter (queue[1]) so no warp strings several hubs together — with a
-  // small group that chain was the whole launch (Products G = 2: level 1
-  // 160 us, ten top hubs in the first warp).  The PRNG variants' per-node
-  // cost does not grow with the degree (Floyd draws T positions).
-  const unsigned hub_items = kVariants ? 0u : min(items, hub_cap);
-  bool hub_phase = hub_items > 0;
+  // Claim c takes items c, c + M, c + 2M, ... (M = number of claims) of
+  // the rank-major order: each claim holds one item of every tenth of the
+  // ranks, so the lowest ranks — the hubs (frontiers are id-sorted and the
+  // generator's hubs have low ids) — land one per claim, in the first
+  // claims.  Contiguous claims strung several top hubs through one warp
+  // when the group is small (Products G = 2: level 1 160 us, the ten top
+  // hubs in the first claim).
+  const unsigned nclaims = (items + claim - 1) / claim;
   for (;;) {
-    unsigned t0 = 0, n = claim;
-    if (hub_phase) {
-      if (lane == 0) t0 = atomicAdd(queue + 1, 1u);
-      t0 = __shfl_sync(kFull, t0, 0);
-      if (t0 < hub_items)
-        n = 1;
-      else
-        hub_phase = false;
-    }
-    if (!hub_phase) {
-      if (lane == 0) t0 = atomicAdd(queue, claim);
-      t0 = __shfl_sync(kFull, t0, 0) + hub_items;
-      if (t0 >= items) break;
-    }
+    unsigned t0 = 0;
+    if (lane == 0) t0 = atomicAdd(queue, claim);
+    t0 = __shfl_sync(kFull, t0, 0);
+    if (t0 >= items) break;
     // phase A, one item per lane: decode, meta load and count for the
     // claim's items at once (and, for the PRNG variants, Floyd's draws in
     // the lane's own generator: they are sequential per node, so a
     // warp-uniform generator would run them 32 times over)
-    const unsigned k = t0 + lane;
+    const unsigned k = (unsigned)lane * nclaims + t0 / claim;
     bool live = false;
     int D = 0, b = 0;
     int32_t v = 0;
     int64_t row = 0, a = 0;
-    if (k < items && lane < (int)n) {
+    if (lane < (int)claim && k < items) {
       const int j = (int)(k / (unsigned)G);
       b = (int)(k - (unsigned)j * (unsigned)G);
       if (j < (b < kQueueBatches ? s_nf[b] : __ldg(nfront + b))) {
@@ -907,7 +896,7 @@ extern "C" int rg_sample_level(const int64_t* d_indptr, const int32_t* d_indices
   int4* meta = reinterpret_cast<int4*>(d_meta);
   // launch-wide work queue: the extra record after the G*cap_in meta records
   unsigned* queue = reinterpret_cast<unsigned*>(meta + (int64_t)G * cap_in);
-  if (cudaMemsetAsync(queue, 0, 2 * sizeof(unsigned), s) != cudaSuccess)
+  if (cudaMemsetAsync(queue, 0, sizeof(unsigned), s) != cudaSuccess)
     return check_launch("sample_level queue");
   {
     const int bx = (int)std::min<int64_t>((cap_in + 255) / 256, std::max(1, kNumSMs * 16 / G));
@@ -930,18 +919,14 @@ extern "C" int rg_sample_level(const int64_t* d_indptr, const int32_t* d_indices
     const char* e = getenv("RG_SAMPLER_VCTAS");
     return e ? std::max(1, std::min(5, atoi(e))) : 5;
   }();
-  static const unsigned hub_cap = [] {
-    const char* e = getenv("RG_SAMPLER_HUB_ITEMS");
-    return e ? (unsigned)std::max(0, atoi(e)) : kHubItems;
-  }();
   if (prng == kSplitMix)
     sample_level_kernel<false><<<kNumSMs * 5, kSampleWarps * 32, 0, s>>>(
         d_indptr, d_indices, G, d_front, meta, cap_in, d_nfront, fanout, level_mix, d_rng_seed,
-        d_ell, d_cnt, d_bm, nwords, slow, sorted_rows, prng, queue, claim, hub_cap);
+        d_ell, d_cnt, d_bm, nwords, slow, sorted_rows, prng, queue, claim);
   else
     sample_level_kernel<true><<<kNumSMs * vctas, kSampleWarps * 32, 0, s>>>(
         d_indptr, d_indices, G, d_front, meta, cap_in, d_nfront, fanout, level_mix, d_rng_seed,
-        d_ell, d_cnt, d_bm, nwords, slow, sorted_rows, prng, queue, vclaim, 0u);
+        d_ell, d_cnt, d_bm, nwords, slow, sorted_rows, prng, queue, vclaim);
   int rc = check_launch("sample_level");
   if (rc || !slow) return rc;
   sample_slow_kernel<<<kNumSMs, 256, 0, s>>>(d_indptr, d_indices, G, d_front, cap_in, fanout,
