@@ -815,6 +815,27 @@ def test_training_run_matches_reference_records(rg, golden, mode, tmp_path):
         assert [c.nodes_pulled for c in csv_rec] == [x.nodes_pulled for x in r.records]
 
 
+@pytest.mark.parametrize("precision", ["f32", "f64"])
+def test_graph_trainer_matches_eager_step(rg, golden, precision):
+    """The graph-captured training step (model.GraphTrainer: chunked weight
+    gradients, rg_softmax_xent, rg_sgd_apply, accumulating-GEMM bias) equals
+    the eager loss_and_grad + sgd_step path (model.py:107-146) up to the
+    fp32 summation order: per-epoch losses within rel 1e-5 (f64: 1e-10),
+    final parameters within the same tolerance."""
+    from paper_2505_10806_b200.train import RunConfig, run
+
+    base = dict(golden["replay"]["config"], epochs=2, precision=precision)
+    a = run(RunConfig(**base, mode="rapid", cuda_graphs=True))
+    b = run(RunConfig(**base, mode="rapid", cuda_graphs=False))
+    rel = 1e-5 if precision == "f32" else 1e-10
+    for ra, rb in zip(a, b):
+        for xa, xb in zip(ra.records, rb.records):
+            assert xa.loss == pytest.approx(xb.loss, rel=rel)
+        for pa, pb in zip(ra.params, rb.params):
+            for ta, tb in ((pa.w_self, pb.w_self), (pa.w_neigh, pb.w_neigh), (pa.bias, pb.bias)):
+                assert torch.allclose(ta, tb, rtol=rel * 10, atol=rel)
+
+
 def test_training_mode_equivalence(rg, golden):
     """Criterion 3 of the reference acceptance suite (test_acceptance.py:113-122):
     rapid and baseline consume bit-identical rows, so losses, accuracies and
