@@ -605,12 +605,14 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
     n_batches = len(timed_batches)
-    # our kernels per step: fill_seeds, mark_seeds, 2 compaction, per level
-    # (node_meta, sample_level, 2 compaction), gather; + 5 for the group
-    # prefetch (kind bits, union, 2 compaction, row copy) when it gathers rows
-    # (dense groups copy whole shards with cudaMemcpyAsync: no kernels)
-    pf_kernels = 5 if pipe.prefetch and getattr(pipe, "pf_mode", "rows") == "rows" else 0
-    gpu_launches = args.steps * (5 + 4 * smp.L + pf_kernels)
+    # our kernels per step: fill_seeds, mark_seeds, a compaction, per level
+    # (node_meta, sample_level, a compaction), gather; + the group prefetch
+    # (kind bits, union, a compaction, row copy) when it gathers rows (dense
+    # groups copy whole shards with cudaMemcpyAsync: no kernels).  A
+    # compaction is 2 launches, 3 with a separate chunk scan (large n)
+    c = int(_lib.load().rg_bitmap_compact_launches(dg.nwords))
+    pf_kernels = 3 + c if pipe.prefetch and getattr(pipe, "pf_mode", "rows") == "rows" else 0
+    gpu_launches = args.steps * (3 + c + smp.L * (2 + c) + pf_kernels)
 
     # full-epoch accounting pass (remote rows/epoch, parity metric)
     pipe.start_epoch(sched, 0)

@@ -121,6 +121,9 @@ int rg_prng_select(int32_t kind, uint64_t nk, uint64_t sd, int32_t D, int32_t T,
  * If d_wpre != NULL it also receives the exclusive popcount prefix per
  * word (G x nwords), i.e. rank(v) = wpre[v>>5] + popc(bm & lowmask). */
 int64_t rg_bitmap_chunks(int64_t nwords);
+/* kernel launches one rg_bitmap_compact call makes (2, or 3 when the chunk
+ * totals get their own scan kernel: more than 256 chunks)               */
+int rg_bitmap_compact_launches(int64_t nwords);
 int rg_bitmap_compact(const uint32_t* d_bm, int64_t nwords, int32_t G, int32_t* d_chunk,
                       int32_t* d_out, int64_t cap_out, int32_t* d_nout, int32_t* d_wpre,
                       void* stream);

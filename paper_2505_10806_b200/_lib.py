@@ -47,6 +47,7 @@ _SIGNATURES = {
     "rg_sample_level": (c_int32, [P, P, c_int64, c_int32, P, c_int64, P, c_int32, c_int32, P, P,
                                   P, P, c_int64, P, P, c_int32, c_int32, P]),
     "rg_bitmap_chunks": (c_int64, [c_int64]),
+    "rg_bitmap_compact_launches": (c_int32, [c_int64]),
     "rg_bitmap_compact": (c_int32, [P, c_int64, c_int32, P, P, c_int64, P, P, P]),
     "rg_bitmap_set": (c_int32, [P, P, P, P]),
     "rg_scan_chunks": (c_int64, [c_int64]),

@@ -692,13 +692,40 @@ __global__ void __launch_bounds__(kCompactThreads)
   if (threadIdx.x == 0) chunk_tot[(int64_t)b * nchunks + blockIdx.x] = tot;
 }
 
+// Exclusive prefix of the chunk totals per batch, in place, and the batch
+// total: one CTA per batch.  Used when there are many chunks (papers100M
+// shape: ~3,400 per batch); with few, the emit kernel sums the totals before
+// its chunk itself (one pass, no extra launch).
+constexpr int64_t kEmitScanMax = 256;
+constexpr int kChunkScanThreads = 1024;
+
+__global__ void __launch_bounds__(kChunkScanThreads)
+    chunk_scan_kernel(int32_t* __restrict__ chunk, int64_t nchunks, int32_t* __restrict__ nout) {
+  __shared__ int s_red[32];
+  int32_t* c = chunk + (int64_t)blockIdx.x * nchunks;
+  int carry = 0;
+  for (int64_t base = 0; base < nchunks; base += kChunkScanThreads) {
+    const int64_t i = base + threadIdx.x;
+    const int v = i < nchunks ? c[i] : 0;
+    int tot;
+    const int ex = block_excl_scan<kChunkScanThreads>(v, s_red, &tot);
+    if (i < nchunks) c[i] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) nout[blockIdx.x] = carry;
+}
+
 // Emission is warp-cooperative: each warp owns kCompactWords/8 consecutive
 // words; for every word the 32 lanes test one bit each and the set bits are
 // written with one coalesced store (ballot + prefix popcount).
+// prescanned: chunk_tot already holds exclusive prefixes (chunk_scan_kernel,
+// which also wrote nout); else every CTA sums the totals before its chunk
+// (quadratic in the chunk count: only for few chunks).
 __global__ void __launch_bounds__(kCompactThreads)
     bitmap_emit_kernel(const uint32_t* __restrict__ bm, int64_t nwords, int64_t nchunks,
                        const int32_t* __restrict__ chunk_tot, int32_t* __restrict__ out,
-                       int64_t cap_out, int32_t* __restrict__ nout, int32_t* __restrict__ wpre) {
+                       int64_t cap_out, int32_t* __restrict__ nout, int32_t* __restrict__ wpre,
+                       int prescanned) {
   constexpr int kWarps = kCompactThreads / 32;
   constexpr int kPerWarp = kCompactWords / kWarps;  // 128 words
   __shared__ int s_red[32];
@@ -708,20 +735,25 @@ __global__ void __launch_bounds__(kCompactThreads)
   const int b = blockIdx.y;
   const int64_t chunk = blockIdx.x;
   const int lane = lane_id(), warp = threadIdx.x >> 5;
-  int before = 0, all = 0;
-  for (int64_t c = threadIdx.x; c < nchunks; c += blockDim.x) {
-    const int t = chunk_tot[(int64_t)b * nchunks + c];
-    all += t;
-    if (c < chunk) before += t;
-  }
-  int tot;
-  block_excl_scan<kCompactThreads>(before, s_red, &tot);
-  if (threadIdx.x == 0) s_base = tot;
-  __syncthreads();
-  if (chunk == 0) {
-    int grand;
-    block_excl_scan<kCompactThreads>(all, s_red, &grand);
-    if (threadIdx.x == 0) nout[b] = grand;
+  if (prescanned) {
+    if (threadIdx.x == 0) s_base = chunk_tot[(int64_t)b * nchunks + chunk];
+    __syncthreads();
+  } else {
+    int before = 0, all = 0;
+    for (int64_t c = threadIdx.x; c < nchunks; c += blockDim.x) {
+      const int t = chunk_tot[(int64_t)b * nchunks + c];
+      all += t;
+      if (c < chunk) before += t;
+    }
+    int tot;
+    block_excl_scan<kCompactThreads>(before, s_red, &tot);
+    if (threadIdx.x == 0) s_base = tot;
+    __syncthreads();
+    if (chunk == 0) {
+      int grand;
+      block_excl_scan<kCompactThreads>(all, s_red, &grand);
+      if (threadIdx.x == 0) nout[b] = grand;
+    }
   }
   const uint32_t* w = bm + (int64_t)b * nwords;
   const int64_t wbase = chunk * kCompactWords + (int64_t)warp * kPerWarp;
@@ -944,6 +976,10 @@ extern "C" int64_t rg_bitmap_chunks(int64_t nwords) {
   return (nwords + kCompactWords - 1) / kCompactWords;
 }
 
+extern "C" int rg_bitmap_compact_launches(int64_t nwords) {
+  return rg_bitmap_chunks(nwords) > kEmitScanMax ? 3 : 2;
+}
+
 extern "C" int rg_bitmap_compact(const uint32_t* d_bm, int64_t nwords, int32_t G,
                                  int32_t* d_chunk, int32_t* d_out, int64_t cap_out,
                                  int32_t* d_nout, int32_t* d_wpre, void* stream) {
@@ -955,8 +991,13 @@ extern "C" int rg_bitmap_compact(const uint32_t* d_bm, int64_t nwords, int32_t G
   bitmap_count_kernel<<<grid, kCompactThreads, 0, s>>>(d_bm, nwords, nchunks, d_chunk);
   int rc = check_launch("bitmap_count");
   if (rc) return rc;
+  const int prescanned = nchunks > kEmitScanMax;
+  if (prescanned) {
+    chunk_scan_kernel<<<G, kChunkScanThreads, 0, s>>>(d_chunk, nchunks, d_nout);
+    if ((rc = check_launch("chunk_scan"))) return rc;
+  }
   bitmap_emit_kernel<<<grid, kCompactThreads, 0, s>>>(d_bm, nwords, nchunks, d_chunk, d_out,
-                                                      cap_out, d_nout, d_wpre);
+                                                      cap_out, d_nout, d_wpre, prescanned);
   return check_launch("bitmap_emit");
 }
 

@@ -85,6 +85,7 @@ class WorkerPipeline:
         self.perm: torch.Tensor | None = None
         self.epoch = 0
         self.launches = 0
+        self._cl = int(_lib.load().rg_bitmap_compact_launches(dg.nwords))  # per compaction
         self.prefetch = False
         self.pf_transport = "p2p"
         self.timeline: list | None = None  # [(name, slot, start ev, end ev)] when set
@@ -177,7 +178,7 @@ class WorkerPipeline:
         _lib.call("rg_prefetch_rows", ptr(self.pf_ids), nid, st.n, ptr(route),
                   bases_array(st.bases), bases_array(dst), st.src_stride, st.stride, s)
         self.pf_rows += self.pf_n[slot]
-        self.launches += 6
+        self.launches += 3 + self._cl
 
     def _exchange_nccl(self, ng: int, smp, slot: int, route, dst) -> None:
         """NCCL transport: requested ids to their owners, rows back, scatter
@@ -279,7 +280,7 @@ class WorkerPipeline:
         self.plan.fill(self.perm, self.epoch, i0, ng)
         smp.run(ng)
         self.gather(ng, i0)
-        self.launches += 1 + 1 + 2 + smp.L * 3 + 1
+        self.launches += 3 + self._cl + smp.L * (2 + self._cl)
         return ng
 
     def step_graph(self, i0: int) -> int:
@@ -359,7 +360,7 @@ class WorkerPipeline:
             self.gather(ng, i0, smp, self.row_bufs[slot], slot=slot, prefetched=True)
             mark("gather", self.s_gather, e2)
             self.ev_gathered[slot].record(self.s_gather)
-        self.launches += 1 + 1 + 2 + smp.L * 3 + 1
+        self.launches += 3 + self._cl + smp.L * (2 + self._cl)
         return ng
 
     def acquire(self, slot: int) -> None:

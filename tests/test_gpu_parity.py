@@ -473,6 +473,42 @@ def test_sage_mean_strided_rows(rg):
     assert np.array_equal(hself.cpu().numpy(), want_self)
 
 
+@pytest.mark.parametrize("nbits", [3_000_000, 12_000_000])
+def test_bitmap_compact_both_scan_paths(rg, nbits):
+    """rg_bitmap_compact (np.unique / np.union1d, sampler.py:138,148) on G = 3
+    bitmaps: below and above the chunk count where the chunk totals get their
+    own scan kernel (papers100M-sized node sets); ids, counts and the per-word
+    ranks wpre equal numpy's."""
+    from paper_2505_10806_b200 import _lib
+
+    lib = _lib.load()
+    G = 3
+    nwords = (nbits + 31) // 32
+    assert (lib.rg_bitmap_compact_launches(nwords) == 3) == (nbits > 8_388_608)
+    rng = np.random.default_rng(nbits)
+    dens = [0.001, 0.05, 0.3]
+    bits = np.zeros((G, nwords * 32), bool)
+    for b in range(G):
+        bits[b, :nbits] = rng.random(nbits) < dens[b]
+    # bit j of word w = node 32 w + j
+    words = np.packbits(bits.reshape(G, nwords * 32), axis=-1, bitorder="little").view("<u4")
+    cap = int(bits.sum(axis=1).max()) + 1
+    d_bm = torch.from_numpy(words.view(np.int32).copy()).cuda()
+    chunk = torch.empty((G, int(lib.rg_bitmap_chunks(nwords))), dtype=torch.int32, device="cuda")
+    out = torch.empty((G, cap), dtype=torch.int32, device="cuda")
+    nout = torch.empty(G, dtype=torch.int32, device="cuda")
+    wpre = torch.empty((G, nwords), dtype=torch.int32, device="cuda")
+    _lib.call("rg_bitmap_compact", d_bm.data_ptr(), nwords, G, chunk.data_ptr(), out.data_ptr(),
+              cap, nout.data_ptr(), wpre.data_ptr(), _lib.stream_handle())
+    got_n, got, got_pre = nout.cpu().numpy(), out.cpu().numpy(), wpre.cpu().numpy()
+    for b in range(G):
+        ids = np.flatnonzero(bits[b])
+        assert got_n[b] == len(ids)
+        assert np.array_equal(got[b, : len(ids)], ids)
+        pc = bits[b].reshape(nwords, 32).sum(axis=1)
+        assert np.array_equal(got_pre[b], np.concatenate([[0], np.cumsum(pc)[:-1]]))
+
+
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
 def test_softmax_xent_and_sgd_apply(rg, dtype):
     """The training step's fused head and update (rg_softmax_xent,
