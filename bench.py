@@ -81,6 +81,9 @@ def parse():
                          "NCCL all-to-alls, ids out and rows back (nccl; spans nodes)")
     ap.add_argument("--pull", action="store_true",
                     help="N>1: every batch pulls its peer rows over NVLink (no group prefetch)")
+    ap.add_argument("--env-sweep", default="",
+                    help="diagnostic: ';'-separated K=V[,K=V] library knob settings; the timed "
+                         "steps are re-run under each and logged (env_sweep key)")
     ap.add_argument("--graphs", action="store_true",
                     help="replay each group's launches from a captured CUDA graph (serial)")
     return ap.parse_args()
@@ -614,6 +617,38 @@ def main():
     pf_kernels = 3 + c if pipe.prefetch and getattr(pipe, "pf_mode", "rows") == "rows" else 0
     gpu_launches = args.steps * (3 + c + smp.L * (2 + c) + pf_kernels)
 
+    env_sweep = None
+    if args.env_sweep:  # diagnostic: the same timed loop under other library knobs
+        env_sweep = {}
+        for setting in args.env_sweep.split(";"):
+            saved = dict(os.environ)
+            for kv in filter(None, setting.split(",")):
+                key, val = kv.split("=", 1)
+                os.environ[key] = val
+            pipe.enter_streams()
+            for kk in range(2):
+                step(kk)
+            pipe.sync_streams()
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            start.record()
+            pipe.enter_streams()
+            for kk in range(args.steps):
+                step(args.warmup + kk)
+            pipe.sync_streams()
+            end.record()
+            torch.cuda.synchronize()
+            tt = torch.tensor([start.elapsed_time(end)], dtype=torch.float64, device="cuda")
+            if world > 1:
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms = float(tt.item())
+            env_sweep[setting] = {"ms_per_step": ms / args.steps,
+                                  "batches_per_s": world * args.steps * G / (ms / 1e3)}
+            log(f"[bench] env {setting}: {env_sweep[setting]}")
+            os.environ.clear()
+            os.environ.update(saved)
+
     # full-epoch accounting pass (remote rows/epoch, parity metric)
     pipe.start_epoch(sched, 0)
     eev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -758,6 +793,7 @@ def main():
                             "with the gather alone; 770 GB/s = measured peer copy per "
                             "direction (B200_PROFILING.md)"} if world > 1 else None),
         "gpu_launches": gpu_launches,
+        **({"env_sweep": env_sweep} if env_sweep else {}),
         "clocks": clk.summary(),
         "remote_rows_epoch": {"worker": part, "uncached": remote_rows,
                               "fallback": tot["fallback"], "cache_hits": tot["hit"],

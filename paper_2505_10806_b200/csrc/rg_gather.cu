@@ -170,8 +170,9 @@ __global__ void __launch_bounds__(kGatherWarps * 32, 4)
     gather_queue_kernel(const int32_t* __restrict__ ids, const int32_t* __restrict__ nids,
                         int64_t cap, int G, const uint32_t* __restrict__ route,
                         const __grid_constant__ Bases bases, int src_stride, int stride,
-                        int nvec, int dq, int dr, int my_part, float* __restrict__ out,
-                        uint32_t* __restrict__ counters, unsigned* __restrict__ queue) {
+                        int nvec, int dq, int dr, int my_part, uint32_t peer_mask,
+                        float* __restrict__ out, uint32_t* __restrict__ counters,
+                        unsigned* __restrict__ queue) {
   __shared__ uint32_t s_cnt[kQueueMaxG][RG_NCOUNTERS];
   __shared__ int32_t s_nr[kQueueMaxG];
   __shared__ const float* s_base[16];
@@ -223,8 +224,11 @@ __global__ void __launch_bounds__(kGatherWarps * 32, 4)
       const unsigned n_fb = __popc(__ballot_sync(kFull, fb));
       const unsigned n_bad = __popc(__ballot_sync(kFull, bad));
       const unsigned om = __reduce_or_sync(kFull, fb ? (1u << kind) : 0u);
+      const unsigned n_peer =
+          peer_mask ? __popc(__ballot_sync(kFull, fb && ((peer_mask >> kind) & 1u))) : 0u;
       if (lane == 0) {
         uint32_t* sc = s_cnt[b];
+        if (n_peer) atomicAdd(sc + RG_CNT_PEER, n_peer);
         if (n_local) atomicAdd(sc + RG_CNT_LOCAL, n_local);
         if (n_hit) atomicAdd(sc + RG_CNT_HIT, n_hit);
         if (n_fb) atomicAdd(sc + RG_CNT_FALLBACK, n_fb);
@@ -632,19 +636,23 @@ extern "C" int rg_gather_bundle(const int32_t* d_ids, const int32_t* d_nids, int
   // With peer (NVLink) shards the gather is latency-bound on remote reads:
   // 6 CTAs/SM (1.5 waves) measured best at N = 2 (9,355 vs 8,930 batches/s
   // at 3/SM; 8/SM 9,129).
-  static const int env_ctas = [] {
-    const char* e = getenv("RG_GATHER_CTAS_PER_SM");
-    return e ? std::max(1, atoi(e)) : 0;
-  }();
+  // knobs read per call (diagnostic sweeps set them between launches)
+  auto env_int = [](const char* name, int dflt) {
+    const char* e = getenv(name);
+    return e ? atoi(e) : dflt;
+  };
+  const int env_ctas = std::max(0, env_int("RG_GATHER_CTAS_PER_SM", 0));
   const int ctas_per_sm = env_ctas ? env_ctas : (peer_mask ? 6 : 4);
   const int64_t want = (cap + kGatherWarps * 32 - 1) / (kGatherWarps * 32);
   const int gx = (int)std::max<int64_t>(
       1, std::min<int64_t>(want, ((int64_t)kNumSMs * ctas_per_sm) / G));
-  static const bool use_queue = [] {
-    const char* e = getenv("RG_GATHER_QUEUE");
-    return e ? atoi(e) != 0 : true;
-  }();
-  if (peer_mask == 0 && G <= kQueueMaxG && use_queue &&
+  const bool use_queue = env_int("RG_GATHER_QUEUE", 1) != 0;
+  // peer shards: the per-batch row-aligned kernel below.  The queue (opt-in
+  // with RG_GATHER_PEER_QUEUE=1, rows of 32 vectors only, where its
+  // flattened mapping is row-aligned too) measured slower with NVLink rows:
+  // papers100M-shaped N = 2, 1,991 (3 CTAs/SM) / 1,981 (4) vs 2,152 batches/s
+  const bool peer_queue = peer_mask == 0 || (nvec == 32 && env_int("RG_GATHER_PEER_QUEUE", 0));
+  if (peer_queue && G <= kQueueMaxG && use_queue &&
       (uint64_t)G * (uint64_t)((cap + 31) / 32) < (1ull << 32) - kGatherClaim) {
     unsigned* q = queue_slot((cudaStream_t)stream);
     if (!q) return check_launch("gather queue");
@@ -652,8 +660,8 @@ extern "C" int rg_gather_bundle(const int32_t* d_ids, const int32_t* d_nids, int
     // 4 -> 11,753, 2 -> 11,249 batches/s)
     const int qctas = env_ctas ? env_ctas : 3;
     gather_queue_kernel<<<kNumSMs * qctas, kGatherWarps * 32, 0, (cudaStream_t)stream>>>(
-        d_ids, d_nids, cap, G, d_route, bases, src_stride, stride, nvec, dq, dr, my_part, d_out,
-        d_counters, q);
+        d_ids, d_nids, cap, G, d_route, bases, src_stride, stride, nvec, dq, dr, my_part,
+        peer_mask, d_out, d_counters, q);
     return check_launch("gather_queue");
   }
   if (peer_mask != 0)
