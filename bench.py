@@ -81,6 +81,9 @@ def parse():
                          "NCCL all-to-alls, ids out and rows back (nccl; spans nodes)")
     ap.add_argument("--pull", action="store_true",
                     help="N>1: every batch pulls its peer rows over NVLink (no group prefetch)")
+    ap.add_argument("--no-share", action="store_true",
+                    help="N>1: every rank samples every batch of a group itself (default: the "
+                         "ranks split each group's sampling and copy the shares over NVLink)")
     ap.add_argument("--env-sweep", default="",
                     help="diagnostic: ';'-separated K=V[,K=V] library knob settings; the timed "
                          "steps are re-run under each and logged (env_sweep key)")
@@ -105,6 +108,28 @@ def build_inputs(cfg):
     book = partition_edgecut(g, cfg["parts"])
     log(f"[bench] inputs: n={g.num_nodes} E={g.num_edges} in {time.time() - t:.1f}s")
     return g, book
+
+
+def structure_pin(args, g, book):
+    """papers100M shape: the generated CSR, train mask and LDG owners
+    against the content hashes the C oracle produced in the build container
+    (tests/golden/papers100m.json, tests/golden/make_golden_papers100m.py);
+    None for shapes pinned elsewhere (tests/test_host_native.py)."""
+    import hashlib
+
+    f = ROOT / "tests" / "golden" / f"{args.config}.json"
+    if args.config != "papers100m" or not f.exists():
+        return None
+    want = json.loads(f.read_text())["hash"]
+
+    def h(a):
+        return hashlib.blake2b(np.ascontiguousarray(a).tobytes(), digest_size=16).hexdigest()
+
+    got = {"indptr": h(np.asarray(g.indptr, dtype="<i8")),
+           "indices": h(np.asarray(g.indices, dtype="<i4")),
+           "train_mask": h(np.asarray(g.train_mask, dtype="u1")),
+           "owner": h(np.asarray(book.owner, dtype="u1"))}
+    return got == want
 
 
 def build_inputs_oracle(cfg):
@@ -443,6 +468,7 @@ def main():
     from paper_2505_10806_b200 import multigpu
 
     g, book = build_inputs(cfg)
+    pin = structure_pin(args, g, book) if args.check else None
     k, d = cfg["parts"], cfg["d"]
     if world > k:
         raise SystemExit(f"--gpus {world} > partitions {k}")
@@ -476,6 +502,8 @@ def main():
     sched = SeedSchedule(S0, 1, nb)
     if world > 1 and not args.pull:
         pipe.enable_prefetch(args.transport, rank, world)  # before the cache fill (nccl)
+    if world > 1 and not args.no_share and not args.serial and not args.graphs:
+        pipe.enable_shared_sampling(rank, world)
 
     # per-epoch part: plan pass (access counts), hot set, cache fill
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -686,9 +714,19 @@ def main():
         e2e = run_e2e(pipe, g, cfg, args, world)
 
     result = None
+    shared_check = None
+    if getattr(pipe, "shared", False):
+        if pipe.shared_status():
+            raise SystemExit(f"rank {rank}: a shared-sampling wait timed out")
+        shared_check = verify_shared(pipe, dist) if args.check else None
     check = run_check(pipe, g, cfg, S0, args.prng) if args.check else None
+    if check is not None and shared_check is not None:
+        check["shared_sampling_bit_exact"] = shared_check
+    if check is not None and pin is not None:
+        check["structure_pinned"] = pin
     if check is not None and world > 1:
-        flags = torch.tensor([int(check["blocks_bit_exact"] and check["rows_bit_exact"])],
+        flags = torch.tensor([int(check["blocks_bit_exact"] and check["rows_bit_exact"]
+                                  and check.get("shared_sampling_bit_exact", True))],
                              device="cuda")
         dist.all_reduce(flags, op=dist.ReduceOp.MIN)
         check["all_ranks_bit_exact"] = bool(flags.item())
@@ -805,6 +843,43 @@ def main():
     emit(line)
     if world > 1:
         dist.destroy_process_group()
+
+
+def verify_shared(pipe, dist) -> bool:
+    """A group produced with shared sampling (this rank sampled its share,
+    the peers' shares copied over NVLink) equals the same group sampled
+    entirely on this GPU: every batch's input set (the bitmap for the
+    window gather, the id list otherwise) and bundle rows.  The shared
+    group lands in slot 1, the local one in slot 0 (no copies of the
+    bundles needed)."""
+    import torch
+
+    torch.cuda.synchronize()
+    dist.barrier()
+    pipe.enter_streams()
+    ng = pipe.step_overlapped(0)
+    if pipe.last_slot != 1:
+        ng = pipe.step_overlapped(0)
+    pipe.sync_streams()
+    torch.cuda.synchronize()
+    dist.barrier()  # every peer finished copying from this rank's buffers
+    sh, loc = pipe.samplers[1], pipe.samplers[0]
+    pipe.step(0)  # the same group sampled locally into slot 0
+    torch.cuda.synchronize()
+    L = sh.L
+    dense = pipe._window_gather(ng)
+    nf = loc.nfront[L, :ng].cpu()
+    ok = True
+    for b in range(ng):
+        n = int(nf[b])
+        if dense:
+            ok = ok and torch.equal(sh.bm[b], loc.bm[b]) and torch.equal(sh.wpre[b], loc.wpre[b])
+        else:
+            ok = ok and int(sh.nfront[L, b]) == n
+            ok = ok and torch.equal(sh.front[L][b, :n], loc.front[L][b, :n])
+        ok = ok and torch.equal(pipe.row_bufs[1][b, :n], pipe.row_bufs[0][b, :n])
+    dist.barrier()
+    return bool(ok)
 
 
 def run_check(pipe, g, cfg, s0, prng="splitmix"):

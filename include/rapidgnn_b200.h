@@ -207,6 +207,18 @@ int rg_gather_window(const uint32_t* d_bm, const int32_t* d_wpre, int64_t nwords
  * group prefetch for dense groups.                                       */
 int rg_copy_bytes(void* d_dst, const void* d_src, int64_t nbytes, void* stream);
 
+/* Cross-GPU group sequence counters for shared sampling (N > 1; DESIGN.md
+ * §7).  Every worker samples every batch (train.py:291-311), so the ranks
+ * split a group's batches and copy each other's sampled input sets over
+ * NVLink.  rg_flag_signal: after the stream's earlier work, publish
+ * *d_flag = value (system-scope release).  rg_flag_wait: the stream waits
+ * until *d_flag >= value (d_flag may be a peer GPU's IPC mapping; acquire
+ * loads); after timeout_ms it gives up and sets *d_status = 1 instead of
+ * hanging.                                                                */
+int rg_flag_signal(uint64_t* d_flag, uint64_t value, void* stream);
+int rg_flag_wait(const uint64_t* d_flag, uint64_t value, int32_t timeout_ms, int32_t* d_status,
+                 void* stream);
+
 /* ---- group prefetch of peer rows (north_star item 4) ---
  * bits[w] bit j = the route kind of node 32w+j is in kind_mask.         */
 int rg_route_kind_bits(const uint32_t* d_route, int64_t n, uint32_t kind_mask, uint32_t* d_bits,

@@ -64,6 +64,8 @@ _SIGNATURES = {
     "rg_gather_window": (c_int32, [P, P, c_int64, c_int32, c_int64, P, P, c_int32, c_int32,
                                    c_int32, c_uint32, P, P, P]),
     "rg_copy_bytes": (c_int32, [P, P, c_int64, P]),
+    "rg_flag_signal": (c_int32, [P, c_uint64, P]),
+    "rg_flag_wait": (c_int32, [P, c_uint64, c_int32, P, P]),
     "rg_softmax_xent": (c_int32, [c_int32, P, c_int32, c_int64, P, P, P, P, P, P, P]),
     "rg_sgd_apply": (c_int32, [c_int32, c_int32, P, P, P, P, c_double, P]),
     "rg_route_kind_bits": (c_int32, [P, c_int64, c_uint32, P, P]),

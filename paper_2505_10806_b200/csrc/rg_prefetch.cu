@@ -222,3 +222,56 @@ extern "C" int rg_scatter_rows(const int32_t* d_ids, int64_t n, const uint32_t* 
                                                             (d + 3) / 4);
   return check_launch("scatter_rows");
 }
+
+// ---- cross-GPU group sequence flags (shared sampling) ------
+// Every worker samples every batch (train.py:291-311), so at N > 1 the
+// ranks split each group's batches, sample their share and copy the others'
+// sampled input sets from the peers over NVLink.  A rank publishes "group
+// seq of slot s is sampled / copied" as a 64-bit counter in its own memory;
+// peers poll it through the IPC mapping.  Writes of the kernels before the
+// signal (stream order) are made visible system-wide before the counter;
+// the wait is bounded (a stuck peer sets *d_status instead of hanging the
+// GPU).
+namespace rg {
+namespace {
+__global__ void flag_signal_kernel(unsigned long long* flag, unsigned long long value) {
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(value) : "memory");
+}
+
+__global__ void flag_wait_kernel(const unsigned long long* flag, unsigned long long value,
+                                 long long timeout_cycles, int32_t* status) {
+  const long long t0 = clock64();
+  for (;;) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+    if (v >= value) break;
+    if (clock64() - t0 > timeout_cycles) {
+      atomicExch(status, 1);
+      break;
+    }
+    __nanosleep(256);
+  }
+  __threadfence_system();
+}
+}  // namespace
+}  // namespace rg
+
+extern "C" int rg_flag_signal(uint64_t* d_flag, uint64_t value, void* stream) {
+  RG_REQUIRE(d_flag != nullptr && ((uintptr_t)d_flag & 7) == 0, "rg_flag_signal: bad flag");
+  flag_signal_kernel<<<1, 1, 0, (cudaStream_t)stream>>>((unsigned long long*)d_flag, value);
+  return check_launch("flag_signal");
+}
+
+extern "C" int rg_flag_wait(const uint64_t* d_flag, uint64_t value, int32_t timeout_ms,
+                            int32_t* d_status, void* stream) {
+  RG_REQUIRE(d_flag != nullptr && ((uintptr_t)d_flag & 7) == 0 && d_status != nullptr &&
+                 timeout_ms > 0,
+             "rg_flag_wait: bad arguments");
+  // ~2 GHz SM clock: cycles per ms, generous (the bound only has to stop a hang)
+  const long long cycles = (long long)timeout_ms * 2000000ll;
+  flag_wait_kernel<<<1, 1, 0, (cudaStream_t)stream>>>((const unsigned long long*)d_flag, value,
+                                                      cycles, d_status);
+  return check_launch("flag_wait");
+}
+

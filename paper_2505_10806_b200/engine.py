@@ -179,23 +179,32 @@ class BlockSampler:
         self.nseeds[b: b + 1].copy_(dev[2:3])
         self.seeds[b, :n].copy_(dev[3:])
 
-    def run(self, ngroup: int | None = None) -> None:
-        """Sample all L levels for slots [0, ngroup) on the current stream."""
-        G = self.G if ngroup is None else int(ngroup)
+    def run(self, ngroup: int | None = None, b0: int = 0) -> None:
+        """Sample all L levels for slots [b0, ngroup) on the current stream
+        (b0 > 0: one rank's share of a group under shared sampling; every
+        per-slot array is slot-major, so the share is a pointer offset)."""
+        G = (self.G if ngroup is None else int(ngroup)) - int(b0)
+        if G <= 0:
+            return
         dg, s = self.dg, _cur()
-        self.bm[:G].zero_()
-        _lib.call("rg_mark_seeds", ptr(self.seeds), ptr(self.nseeds), G, self.caps[0],
-                  ptr(self.bm), dg.nwords, s)
-        _lib.call("rg_bitmap_compact", ptr(self.bm), dg.nwords, G, ptr(self.chunk),
-                  ptr(self.front[0]), self.caps[0], ptr(self.nfront[0]), None, s)
+
+        def o(t):  # slot b0 of a slot-major tensor
+            return ptr(t) + int(b0) * t.stride(0) * t.element_size()
+
+        nf = [ptr(self.nfront) + 4 * (d * self.G + int(b0)) for d in range(self.L + 1)]
+        self.bm[b0:b0 + G].zero_()
+        _lib.call("rg_mark_seeds", o(self.seeds), o(self.nseeds), G, self.caps[0],
+                  o(self.bm), dg.nwords, s)
+        _lib.call("rg_bitmap_compact", o(self.bm), dg.nwords, G, ptr(self.chunk),
+                  o(self.front[0]), self.caps[0], nf[0], None, s)
         for d in range(self.L):
             _lib.call("rg_sample_level", ptr(dg.indptr), ptr(dg.indices), dg.n, G,
-                      ptr(self.front[d]), self.caps[d], ptr(self.nfront[d]), self.step_fan[d], d,
-                      ptr(self.rng), ptr(self.ell[d]), ptr(self.cnt[d]), ptr(self.bm), dg.nwords,
+                      o(self.front[d]), self.caps[d], nf[d], self.step_fan[d], d,
+                      o(self.rng), o(self.ell[d]), o(self.cnt[d]), o(self.bm), dg.nwords,
                       ptr(self.slow), ptr(self.meta), int(dg.sorted_rows), self.prng_code, s)
-            _lib.call("rg_bitmap_compact", ptr(self.bm), dg.nwords, G, ptr(self.chunk),
-                      ptr(self.front[d + 1]), self.caps[d + 1], ptr(self.nfront[d + 1]),
-                      ptr(self.wpre) if d == self.L - 1 else None, s)
+            _lib.call("rg_bitmap_compact", o(self.bm), dg.nwords, G, ptr(self.chunk),
+                      o(self.front[d + 1]), self.caps[d + 1], nf[d + 1],
+                      o(self.wpre) if d == self.L - 1 else None, s)
 
     def edges(self, d: int, ngroup: int | None = None):
         """Flat (src, dst) of level d for every slot: (src, dst, nedge) device."""

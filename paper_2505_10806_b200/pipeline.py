@@ -151,6 +151,97 @@ class WorkerPipeline:
         self.pf_whole_shards = os.environ.get("RG_PREFETCH_WHOLE", "1") != "0"
         self.prefetch = bool(peers)
 
+    # -- shared sampling (multi-GPU) ------------------------------------------
+    def enable_shared_sampling(self, rank: int, world: int, timeout_ms: int = 20000) -> None:
+        """Split each group's sampling across the ranks.  Every worker
+        processes every batch (train.py:291-311), so the N ranks sample the
+        same blocks; here rank r samples only slots [r*ng/N, (r+1)*ng/N) of
+        a group and copies the other slots' input sets (the level-L bitmaps
+        + ranks, or id lists, whichever the gather reads) from the peers'
+        sampler buffers over NVLink (copy engine).  Cross-process order by
+        64-bit group sequence counters in each rank's memory polled through
+        the IPC mapping (rg_flag_signal / rg_flag_wait): "slot s holds my
+        share of group k" and "I copied the peers' shares of group k".
+        Bundles and accounting are unchanged (bench --check compares a
+        shared group with a locally sampled one)."""
+        self.rank, self.world = int(rank), int(world)
+        if self.world < 2:
+            return
+        dev = self.dg.device
+        self.sh_flags = torch.zeros((2, self.nbuf), dtype=torch.int64, device=dev)
+        self.sh_status = torch.zeros(1, dtype=I32, device=dev)
+        self.sh_timeout = int(timeout_ms)
+        tensors = [self.sh_flags]
+        for smp in self.samplers:
+            tensors += [smp.bm, smp.wpre, smp.front[smp.L], smp.nfront]
+        ptrs = multigpu.exchange_buffers(tensors, self.rank, self.world)
+        self.sh_peer_flags = ptrs[0]
+        self.sh_peer_bufs = [ptrs[1 + 4 * i: 5 + 4 * i] for i in range(self.nbuf)]
+        self.shared = True
+        self.sh_seq = 0
+        self.sh_last = [0] * self.nbuf  # sequence number last sampled into each slot
+
+    def _share_range(self, ng: int, r: int) -> tuple[int, int]:
+        return r * ng // self.world, (r + 1) * ng // self.world
+
+    def _sample_shared(self, ng: int, smp, slot: int, seq: int) -> None:
+        """Current stream: sample my share of the group into `slot`, publish
+        it, copy the peers' shares (what the gather reads), publish that."""
+        s = _lib.stream_handle()
+        fl = ptr(self.sh_flags)
+        # the peers finished copying the previous group held in this slot
+        prev = self.sh_last[slot]
+        self.sh_last[slot] = seq
+        if prev > 0:
+            for r in range(self.world):
+                if r != self.rank:
+                    _lib.call("rg_flag_wait", self.sh_peer_flags[r] + 8 * (self.nbuf + slot),
+                              prev, self.sh_timeout, ptr(self.sh_status), s)
+        b0, b1 = self._share_range(ng, self.rank)
+        smp.run(b1, b0=b0)
+        _lib.call("rg_flag_signal", fl + 8 * slot, seq, s)
+        nw = self.dg.nwords
+        # what this group's consumers read: the window gather the bitmaps +
+        # ranks, the id-list gather front[L] / nfront[L], a row-wise or NCCL
+        # group prefetch the bitmaps (the group union)
+        window = self._window_gather(ng)
+        whole = (self.pf_transport == "p2p" and getattr(self, "pf_whole_shards", True)
+                 and ng * self.cap_in >= 4 * self.dg.n)
+        need = [window or (self.prefetch and not whole), window, not window, not window]
+        local = self.sh_peer_bufs[slot]
+        for r in range(self.world):
+            if r == self.rank:
+                continue
+            c0, c1 = self._share_range(ng, r)
+            if c1 <= c0:
+                continue
+            _lib.call("rg_flag_wait", self.sh_peer_flags[r] + 8 * slot, seq, self.sh_timeout,
+                      ptr(self.sh_status), s)
+            cap = self.cap_in
+            spans = [(4 * c0 * nw, 4 * (c1 - c0) * nw), (4 * c0 * nw, 4 * (c1 - c0) * nw),
+                     (4 * c0 * cap, 4 * (c1 - c0) * cap), (4 * (smp.L * self.G + c0), 4 * (c1 - c0))]
+            for i, (off, nbytes) in enumerate(spans):
+                if need[i]:
+                    _lib.call("rg_copy_bytes", local[i][self.rank] + off, local[i][r] + off,
+                              nbytes, s)
+        _lib.call("rg_flag_signal", fl + 8 * (self.nbuf + slot), seq, s)
+        self.launches += 2 + (self.world - 1) + (1 if prev > 0 else 0) * (self.world - 1)
+
+    def shared_status(self) -> int:
+        """1 if any cross-GPU wait timed out (results then invalid)."""
+        return int(self.sh_status.item()) if getattr(self, "shared", False) else 0
+
+    def _dense(self, ng: int) -> bool:
+        st = self.store
+        return ng * self.cap_in >= 4 * self.dg.n and st.stride * 4 * 32 <= 200 * 1024
+
+    def _window_gather(self, ng: int) -> bool:
+        """True if gather() reads the group's bitmaps + ranks (the staged
+        window gather), False if it reads the id lists."""
+        peer_mask = 0 if self.prefetch else self.store.peer_mask
+        return (self.gather_mode == "window" and self._dense(ng) and ng <= 128
+                and peer_mask == 0)
+
     def _route(self):
         if self.cache is not None and self.cache.hot_ids.numel():
             return self.cache.route
@@ -349,7 +440,11 @@ class WorkerPipeline:
                 smp.seeds.copy_(host_seeds[0], non_blocking=True)
                 smp.nseeds.copy_(host_seeds[1], non_blocking=True)
                 smp.rng.copy_(host_seeds[2], non_blocking=True)
-            smp.run(ng)
+            if getattr(self, "shared", False):
+                self.sh_seq += 1
+                self._sample_shared(ng, smp, slot, self.sh_seq)
+            else:
+                smp.run(ng)
             e1 = mark("sample", self.s_sample, e0)
             if self.prefetch and not self.prefetch_stream:
                 self.prefetch_group(ng, smp, slot)
@@ -421,8 +516,7 @@ class WorkerPipeline:
         # row (Products G = 128: 56, measured ~35 -> 5.97 vs 6.70 ms); for
         # sparse groups (papers100M-shaped, G = 8: 0.31) the id-list queue
         # gather is faster (15.8 vs ~3.5 ms per launch)
-        dense = ng * self.cap_in >= 4 * self.dg.n and st.stride * 4 * 32 <= 200 * 1024
-        if self.gather_mode == "window" and dense and ng <= 128 and peer_mask == 0:
+        if self._window_gather(ng):
             # staged union gather straight from the group's input bitmaps
             self.gather_kernel = "gather_staged_kernel (rg_gather_window)"
             _lib.call("rg_gather_window", ptr(smp.bm), ptr(smp.wpre), self.dg.nwords, ng,

@@ -924,6 +924,8 @@ def test_two_gpu_peer_gather_bit_exact(mode):
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads([x for x in out.stdout.splitlines() if x.startswith("{")][-1])
     assert line["check"]["all_ranks_bit_exact"] is True
+    # the ranks split each group's sampling and copy the shares over NVLink
+    assert line["check"]["shared_sampling_bit_exact"] is True
     assert line["remote_rows_epoch"]["uncached"] == 933_549_256
     assert line["remote_rows_epoch"]["rpcs"] == 11_725
     if mode == "pull":
