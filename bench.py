@@ -590,6 +590,10 @@ def main():
         torch.cuda.synchronize()
         if args.nvtx:
             torch.cuda.nvtx.range_pop()
+    if world > 1:
+        # shared sampling: no rank reuses its sampler buffers (below) while
+        # a peer may still be copying its share of the last timed group
+        dist.barrier()
     step_ms_local = (sum(a.elapsed_time(b) for a, b in sev) if flush
                      else start.elapsed_time(end))
     if pipe.timeline:
