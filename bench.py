@@ -647,7 +647,10 @@ def main():
     # compaction is 2 launches, 3 with a separate chunk scan (large n)
     c = int(_lib.load().rg_bitmap_compact_launches(dg.nwords))
     pf_kernels = 3 + c if pipe.prefetch and getattr(pipe, "pf_mode", "rows") == "rows" else 0
-    gpu_launches = args.steps * (3 + c + smp.L * (2 + c) + pf_kernels)
+    # shared sampling: two counter signals + a wait per peer for its share
+    # and one for its copy of the slot's previous group (copies: copy engine)
+    sh_kernels = 2 + 2 * (world - 1) if getattr(pipe, "shared", False) else 0
+    gpu_launches = args.steps * (3 + c + smp.L * (2 + c) + pf_kernels + sh_kernels)
 
     env_sweep = None
     if args.env_sweep:  # diagnostic: the same timed loop under other library knobs
