@@ -649,7 +649,10 @@ def main():
     pf_kernels = 3 + c if pipe.prefetch and getattr(pipe, "pf_mode", "rows") == "rows" else 0
     # shared sampling: two counter signals + a wait per peer for its share
     # and one for its copy of the slot's previous group (copies: copy engine)
-    sh_kernels = 2 + 2 * (world - 1) if getattr(pipe, "shared", False) else 0
+    # (+ a compaction per peer share re-deriving its input lists when the
+    # bitmaps came over)
+    sh_kernels = (2 + 2 * (world - 1) + (world - 1) * c * int(pipe._window_gather(G))
+                  if getattr(pipe, "shared", False) else 0)
     gpu_launches = args.steps * (3 + c + smp.L * (2 + c) + pf_kernels + sh_kernels)
 
     env_sweep = None
@@ -855,8 +858,9 @@ def main():
 def verify_shared(pipe, dist) -> bool:
     """A group produced with shared sampling (this rank sampled its share,
     the peers' shares copied over NVLink) equals the same group sampled
-    entirely on this GPU: every batch's input set (the bitmap for the
-    window gather, the id list otherwise) and bundle rows.  The shared
+    entirely on this GPU: every batch's whole block (frontiers, counts and
+    ELL edges of every level, the input bitmap and its ranks) and its
+    bundle rows.  The shared
     group lands in slot 1, the local one in slot 0 (no copies of the
     bundles needed)."""
     import torch
@@ -874,16 +878,23 @@ def verify_shared(pipe, dist) -> bool:
     pipe.step(0)  # the same group sampled locally into slot 0
     torch.cuda.synchronize()
     L = sh.L
-    dense = pipe._window_gather(ng)
-    nf = loc.nfront[L, :ng].cpu()
-    ok = True
+    window = pipe._window_gather(ng)
+    nf = loc.nfront[:, :ng].cpu()
+    ok = torch.equal(sh.nfront[:, :ng], loc.nfront[:, :ng])
     for b in range(ng):
-        n = int(nf[b])
-        if dense:
-            ok = ok and torch.equal(sh.bm[b], loc.bm[b]) and torch.equal(sh.wpre[b], loc.wpre[b])
-        else:
-            ok = ok and int(sh.nfront[L, b]) == n
-            ok = ok and torch.equal(sh.front[L][b, :n], loc.front[L][b, :n])
+        n = int(nf[L, b])
+        ok = ok and torch.equal(sh.bm[b], loc.bm[b])
+        if window:
+            ok = ok and torch.equal(sh.wpre[b], loc.wpre[b])
+        for d in range(L + 1):  # every level's frontier
+            ok = ok and torch.equal(sh.front[d][b, : int(nf[d, b])], loc.front[d][b, : int(nf[d, b])])
+        for d in range(L):  # every level's sampled edges (ELL rows up to their counts)
+            m, F = int(nf[d, b]), sh.step_fan[d]
+            cs, cl = sh.cnt[d][b, :m], loc.cnt[d][b, :m]
+            ok = ok and torch.equal(cs, cl)
+            live = torch.arange(F, device=cs.device)[None, :] < cl[:, None].long()
+            es, el = sh.ell[d][b, : m * F].view(m, F), loc.ell[d][b, : m * F].view(m, F)
+            ok = ok and torch.equal(es[live], el[live])
         ok = ok and torch.equal(pipe.row_bufs[1][b, :n], pipe.row_bufs[0][b, :n])
     dist.barrier()
     return bool(ok)

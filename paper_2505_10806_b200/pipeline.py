@@ -156,14 +156,17 @@ class WorkerPipeline:
         """Split each group's sampling across the ranks.  Every worker
         processes every batch (train.py:291-311), so the N ranks sample the
         same blocks; here rank r samples only slots [r*ng/N, (r+1)*ng/N) of
-        a group and copies the other slots' input sets (the level-L bitmaps
-        + ranks, or id lists, whichever the gather reads) from the peers'
-        sampler buffers over NVLink (copy engine).  Cross-process order by
-        64-bit group sequence counters in each rank's memory polled through
-        the IPC mapping (rg_flag_signal / rg_flag_wait): "slot s holds my
-        share of group k" and "I copied the peers' shares of group k".
-        Bundles and accounting are unchanged (bench --check compares a
-        shared group with a locally sampled one)."""
+        a group and copies the other slots' sampled blocks from the peers'
+        sampler buffers over NVLink (copy engine): first what the gather
+        reads (the level-L bitmaps + ranks, or the id lists), which gates the
+        gather, then the rest of every level (frontiers, counts, ELL edges),
+        so each rank ends up holding every batch's whole block, as if it had
+        sampled them all.  Cross-process order by 64-bit group sequence
+        counters in each rank's memory polled through the IPC mapping
+        (rg_flag_signal / rg_flag_wait): "slot s holds my share of group k"
+        and "I copied the peers' shares of group k".  Bundles, blocks and
+        accounting are unchanged (bench --check compares a shared group with
+        a locally sampled one)."""
         self.rank, self.world = int(rank), int(world)
         if self.world < 2:
             return
@@ -171,12 +174,17 @@ class WorkerPipeline:
         self.sh_flags = torch.zeros((2, self.nbuf), dtype=torch.int64, device=dev)
         self.sh_status = torch.zeros(1, dtype=I32, device=dev)
         self.sh_timeout = int(timeout_ms)
+        self.ev_inputs = [torch.cuda.Event() for _ in range(self.nbuf)]
+        self.s_block = torch.cuda.Stream()
+        L = self.sampler.L
         tensors = [self.sh_flags]
         for smp in self.samplers:
-            tensors += [smp.bm, smp.wpre, smp.front[smp.L], smp.nfront]
+            # [bm, wpre, nfront, front 0..L, ell 0..L-1, cnt 0..L-1]
+            tensors += [smp.bm, smp.wpre, smp.nfront, *smp.front, *smp.ell, *smp.cnt]
+        per = 3 + (L + 1) + 2 * L
         ptrs = multigpu.exchange_buffers(tensors, self.rank, self.world)
         self.sh_peer_flags = ptrs[0]
-        self.sh_peer_bufs = [ptrs[1 + 4 * i: 5 + 4 * i] for i in range(self.nbuf)]
+        self.sh_peer_bufs = [ptrs[1 + per * i: 1 + per * (i + 1)] for i in range(self.nbuf)]
         self.shared = True
         self.sh_seq = 0
         self.sh_last = [0] * self.nbuf  # sequence number last sampled into each slot
@@ -184,9 +192,21 @@ class WorkerPipeline:
     def _share_range(self, ng: int, r: int) -> tuple[int, int]:
         return r * ng // self.world, (r + 1) * ng // self.world
 
+    def _share_spans(self, smp, c0: int, c1: int) -> list:
+        """(buffer index, byte offset, bytes) of slots [c0, c1) in every
+        shared sampler buffer, in the enable_shared_sampling order."""
+        L, G = smp.L, self.G
+        rows = [smp.bm, smp.wpre]
+        out = [(i, c0 * t.stride(0) * 4, (c1 - c0) * t.stride(0) * 4) for i, t in enumerate(rows)]
+        out += [(2, 4 * (d * G + c0), 4 * (c1 - c0)) for d in range(L + 1)]  # nfront[d]
+        for i, t in enumerate([*smp.front, *smp.ell, *smp.cnt]):
+            out.append((3 + i, c0 * t.stride(0) * 4, (c1 - c0) * t.stride(0) * 4))
+        return out
+
     def _sample_shared(self, ng: int, smp, slot: int, seq: int) -> None:
         """Current stream: sample my share of the group into `slot`, publish
-        it, copy the peers' shares (what the gather reads), publish that."""
+        it, copy the peers' shares — what the gather reads first (then
+        ev_inputs[slot]), the rest of the blocks after — and publish that."""
         s = _lib.stream_handle()
         fl = ptr(self.sh_flags)
         # the peers finished copying the previous group held in this slot
@@ -200,31 +220,62 @@ class WorkerPipeline:
         b0, b1 = self._share_range(ng, self.rank)
         smp.run(b1, b0=b0)
         _lib.call("rg_flag_signal", fl + 8 * slot, seq, s)
-        nw = self.dg.nwords
-        # what this group's consumers read: the window gather the bitmaps +
+        # what the group's gather reads: the window gather the bitmaps +
         # ranks, the id-list gather front[L] / nfront[L], a row-wise or NCCL
         # group prefetch the bitmaps (the group union)
+        L = smp.L
         window = self._window_gather(ng)
         whole = (self.pf_transport == "p2p" and getattr(self, "pf_whole_shards", True)
                  and ng * self.cap_in >= 4 * self.dg.n)
-        need = [window or (self.prefetch and not whole), window, not window, not window]
+        first = set()
+        if window or (self.prefetch and not whole):
+            first.add((0, 0))  # bm
+        if window:
+            first.add((1, 0))  # wpre
+        else:
+            first.add((2, L))  # nfront[L]
+            first.add((3 + L, 0))  # front[L]
         local = self.sh_peer_bufs[slot]
+        spans = {}
         for r in range(self.world):
-            if r == self.rank:
-                continue
             c0, c1 = self._share_range(ng, r)
-            if c1 <= c0:
+            if r == self.rank or c1 <= c0:
                 continue
             _lib.call("rg_flag_wait", self.sh_peer_flags[r] + 8 * slot, seq, self.sh_timeout,
                       ptr(self.sh_status), s)
-            cap = self.cap_in
-            spans = [(4 * c0 * nw, 4 * (c1 - c0) * nw), (4 * c0 * nw, 4 * (c1 - c0) * nw),
-                     (4 * c0 * cap, 4 * (c1 - c0) * cap), (4 * (smp.L * self.G + c0), 4 * (c1 - c0))]
-            for i, (off, nbytes) in enumerate(spans):
-                if need[i]:
-                    _lib.call("rg_copy_bytes", local[i][self.rank] + off, local[i][r] + off,
-                              nbytes, s)
-        _lib.call("rg_flag_signal", fl + 8 * (self.nbuf + slot), seq, s)
+            spans[r] = self._share_spans(smp, c0, c1)
+        # with the bitmaps copied, the input id lists (front[L], 62 % of a
+        # Products block) are re-derived by a local compaction instead
+        derive = {(2, L), (3 + L, 0)} if window else set()
+
+        def copies(phase, stream):
+            for r, sp in spans.items():
+                nfront_d = 0
+                for i, off, nbytes in sp:
+                    key = (i, nfront_d if i == 2 else 0)
+                    if i == 2:
+                        nfront_d += 1
+                    if (key in first) == (phase == 0) and (i != 1 or window) and key not in derive:
+                        _lib.call("rg_copy_bytes", local[i][self.rank] + off,
+                                  local[i][r] + off, nbytes, stream)
+                if phase == 1 and derive:
+                    c0, c1 = self._share_range(ng, r)
+                    nw, capL = self.dg.nwords, smp.caps[L]
+                    _lib.call("rg_bitmap_compact", ptr(smp.bm) + 4 * c0 * nw, nw, c1 - c0,
+                              ptr(smp.chunk), ptr(smp.front[L]) + 4 * c0 * capL, capL,
+                              ptr(smp.nfront) + 4 * (L * self.G + c0), None, stream)
+                    self.launches += self._cl
+
+        copies(0, s)  # the gather's inputs, on the sampling stream
+        self.ev_inputs[slot].record()
+        # the rest of the blocks on their own stream: the next group's
+        # sampling does not queue behind them
+        with torch.cuda.stream(self.s_block):
+            self.s_block.wait_event(self.ev_inputs[slot])
+            sb = _lib.stream_handle()
+            copies(1, sb)
+            _lib.call("rg_flag_signal", fl + 8 * (self.nbuf + slot), seq, sb)
+            self.ev_sampled[slot].record(self.s_block)
         self.launches += 2 + (self.world - 1) + (1 if prev > 0 else 0) * (self.world - 1)
 
     def shared_status(self) -> int:
@@ -433,6 +484,8 @@ class WorkerPipeline:
 
         with torch.cuda.stream(self.s_sample):
             self.s_sample.wait_event(self.ev_gathered[slot])  # slot free again
+            if getattr(self, "shared", False):  # and the last block copies into it done
+                self.s_sample.wait_event(self.ev_sampled[slot])
             e0 = mark("sample", self.s_sample)
             if host_seeds is None:
                 self.plan.fill(self.perm, self.epoch, i0, ng, smp)
@@ -449,11 +502,14 @@ class WorkerPipeline:
             if self.prefetch and not self.prefetch_stream:
                 self.prefetch_group(ng, smp, slot)
                 mark("prefetch", self.s_sample, e1)
-            self.ev_sampled[slot].record(self.s_sample)
-        gate = self.ev_sampled[slot]
+            if not getattr(self, "shared", False):  # shared: recorded after the block copies
+                self.ev_sampled[slot].record(self.s_sample)
+        # shared sampling: the gather needs only the input sets (the rest of
+        # the peers' blocks is still being copied on its own stream)
+        gate = self.ev_inputs[slot] if getattr(self, "shared", False) else self.ev_sampled[slot]
         if self.prefetch and self.prefetch_stream:
             with torch.cuda.stream(self.s_prefetch):
-                self.s_prefetch.wait_event(self.ev_sampled[slot])
+                self.s_prefetch.wait_event(gate)
                 e3 = mark("prefetch", self.s_prefetch)
                 self.prefetch_group(ng, smp, slot)
                 mark("prefetch", self.s_prefetch, e3)
@@ -470,6 +526,7 @@ class WorkerPipeline:
 
     def acquire(self, slot: int) -> None:
         """Current stream waits until group `slot` is sampled and gathered."""
+        torch.cuda.current_stream().wait_event(self.ev_sampled[slot])
         torch.cuda.current_stream().wait_event(self.ev_gathered[slot])
 
     def release(self, slot: int) -> None:
@@ -480,12 +537,16 @@ class WorkerPipeline:
     def enter_streams(self) -> None:
         """Order both side streams after the current stream's work."""
         cur = torch.cuda.current_stream()
+        if getattr(self, "shared", False):
+            self.s_block.wait_stream(cur)
         self.s_sample.wait_stream(cur)
         self.s_prefetch.wait_stream(cur)
         self.s_gather.wait_stream(cur)
 
     def sync_streams(self) -> None:
         cur = torch.cuda.current_stream()
+        if getattr(self, "shared", False):
+            cur.wait_stream(self.s_block)
         cur.wait_stream(self.s_sample)
         cur.wait_stream(self.s_prefetch)
         cur.wait_stream(self.s_gather)

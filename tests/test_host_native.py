@@ -369,3 +369,52 @@ def test_reference_arm_runs_without_the_product_library():
                                    "cache_pct", "n_hot", "prng"}
     assert line["config"]["n_hot"] == 7125  # int(15 % of worker 0's C1 remote nodes)
     assert line["cpu_baseline"]["kind"] == "port"
+
+
+def test_shared_sampling_spans_cover_exactly_the_share():
+    """Shared sampling copies a peer's share of a group as
+    byte spans of the slot-major sampler buffers: emulating the copies on
+    host tensors moves exactly slots [c0, c1) of every buffer (all levels'
+    frontiers, counts, ELL rows, nfront entries, bitmaps) and nothing else;
+    the shares of N ranks tile the group."""
+    from types import SimpleNamespace
+
+    import torch
+
+    from paper_2505_10806_b200.pipeline import WorkerPipeline
+
+    G, L, nw = 7, 3, 5
+    caps, fan = [4, 12, 40, 90], [2, 3, 2]
+
+    def sampler(fill):
+        g = torch.Generator().manual_seed(fill)
+        r = lambda *shape: torch.randint(-9, 9, shape, generator=g, dtype=torch.int32)
+        return SimpleNamespace(L=L, bm=r(G, nw), wpre=r(G, nw), nfront=r(L + 1, G),
+                               front=[r(G, c) for c in caps],
+                               ell=[r(G, caps[d] * fan[d]) for d in range(L)],
+                               cnt=[r(G, caps[d]) for d in range(L)])
+
+    def bufs(s):
+        return [s.bm, s.wpre, s.nfront, *s.front, *s.ell, *s.cnt]
+
+    for world in (2, 3, 4):
+        me = SimpleNamespace(G=G, world=world)
+        ranges = [WorkerPipeline._share_range(me, G, r) for r in range(world)]
+        assert ranges[0][0] == 0 and ranges[-1][1] == G
+        assert all(a[1] == b[0] for a, b in zip(ranges, ranges[1:]))
+        for c0, c1 in ranges:
+            src, dst = sampler(1), sampler(2)
+            before = [t.clone() for t in bufs(dst)]
+            for i, off, nbytes in WorkerPipeline._share_spans(me, src, c0, c1):
+                s8 = bufs(src)[i].view(-1).view(torch.uint8)
+                d8 = bufs(dst)[i].view(-1).view(torch.uint8)
+                d8[off:off + nbytes] = s8[off:off + nbytes]
+            for k, (a, b, old) in enumerate(zip(bufs(src), bufs(dst), before)):
+                if k == 2:  # nfront [L+1, G]: columns are slots
+                    assert torch.equal(b[:, c0:c1], a[:, c0:c1])
+                    rest = torch.ones(G, dtype=torch.bool)
+                    rest[c0:c1] = False
+                    assert torch.equal(b[:, rest], old[:, rest])
+                else:
+                    assert torch.equal(b[c0:c1], a[c0:c1])
+                    assert torch.equal(b[:c0], old[:c0]) and torch.equal(b[c1:], old[c1:])
