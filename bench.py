@@ -30,6 +30,10 @@ from pathlib import Path
 import numpy as np
 
 ROOT = Path(__file__).resolve().parent
+# more hardware work queues than streams in use: with the default 8, streams
+# alias onto shared queues, and a cross-GPU wait kernel of shared sampling
+# could then hold up an unrelated stream's work (a false dependency)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 sys.path.insert(0, str(ROOT))
 
 METRIC = "sample+fetch mini-batches/s, Products-shape, 1-8 B200; remote rows/epoch"

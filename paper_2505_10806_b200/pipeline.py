@@ -167,22 +167,32 @@ class WorkerPipeline:
         and "I copied the peers' shares of group k".  Bundles, blocks and
         accounting are unchanged (bench --check compares a shared group with
         a locally sampled one)."""
-        self.rank, self.world = int(rank), int(world)
-        if self.world < 2:
+        if int(world) < 2:
             return
+        tensors = self.shared_tensors(rank, world, timeout_ms)
+        self.wire_shared(multigpu.exchange_buffers(tensors, self.rank, self.world))
+
+    def shared_tensors(self, rank: int, world: int, timeout_ms: int = 20000) -> list:
+        """Allocate the shared-sampling counters; returns the buffers every
+        peer maps: [flags] + per slot [bm, wpre, nfront, front 0..L,
+        ell 0..L-1, cnt 0..L-1]."""
+        self.rank, self.world = int(rank), int(world)
         dev = self.dg.device
         self.sh_flags = torch.zeros((2, self.nbuf), dtype=torch.int64, device=dev)
         self.sh_status = torch.zeros(1, dtype=I32, device=dev)
         self.sh_timeout = int(timeout_ms)
         self.ev_inputs = [torch.cuda.Event() for _ in range(self.nbuf)]
         self.s_block = torch.cuda.Stream()
-        L = self.sampler.L
         tensors = [self.sh_flags]
         for smp in self.samplers:
-            # [bm, wpre, nfront, front 0..L, ell 0..L-1, cnt 0..L-1]
             tensors += [smp.bm, smp.wpre, smp.nfront, *smp.front, *smp.ell, *smp.cnt]
+        return tensors
+
+    def wire_shared(self, ptrs: list) -> None:
+        """ptrs[i][r] = address of rank r's shared_tensors()[i] in this
+        process (multigpu.exchange_buffers; the peers' through CUDA IPC)."""
+        L = self.sampler.L
         per = 3 + (L + 1) + 2 * L
-        ptrs = multigpu.exchange_buffers(tensors, self.rank, self.world)
         self.sh_peer_flags = ptrs[0]
         self.sh_peer_bufs = [ptrs[1 + per * i: 1 + per * (i + 1)] for i in range(self.nbuf)]
         self.shared = True

@@ -1000,6 +1000,35 @@ def test_prefetch_kernels_units(rg):
         assert torch.equal(shadow[q][sel.cuda()], shards[q][sel.cuda()])
 
 
+@pytest.mark.parametrize("group", [16, 4])  # dense (window gather) / sparse (id lists)
+def test_shared_sampling_two_workers_one_gpu(group):
+    """Shared sampling without a second GPU: two workers'
+    pipelines in one process, wired to each other's buffers and sequence
+    counters by plain device addresses instead of IPC mappings, produce
+    three groups alternately (slot reuse included), each sampling half of
+    every group and copying the other half.  Every batch's whole block
+    (frontiers, counts, ELL edges, bitmap) and bundle rows equal a pipeline
+    that sampled everything itself, and so do the per-batch counters.
+    Runs in a subprocess with 32 hardware work queues (both workers' streams
+    share one GPU here, and with the default 8 queues a spinning cross-worker
+    wait could alias onto the queue of the work it waits for); the helper
+    loads every kernel before the first wait is in flight and drives each
+    worker from its own host thread, as one process per GPU would (a single
+    thread interleaving both timed out in the id-list mode: a host-side
+    stall while one worker's wait spun kept the other's signal unqueued)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    helper = Path(__file__).with_name("shared_one_gpu.py")
+    env = dict(os.environ, CUDA_DEVICE_MAX_CONNECTIONS="32")
+    out = subprocess.run([sys.executable, str(helper), str(group)], capture_output=True,
+                         text=True, timeout=600, env=env)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-3000:]
+    assert "shared ok" in out.stdout
+
+
 def test_group_prefetch_pipeline_single_gpu(rg, products):
     """The whole group-prefetch path on one GPU: shards 1..7 registered as
     'peer' addresses (set_shard(q, None, base)), so every step copies the
