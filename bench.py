@@ -511,13 +511,18 @@ def main():
 
     # per-epoch part: plan pass (access counts), hot set, cache fill
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    pipe.count_epoch(sched, 0)  # first pass loads modules / warms the allocator
+    share_plan = world > 1 and getattr(pipe, "shared", False)
+    counts_local = pipe.count_epoch(sched, 0)  # first pass loads modules / warms the allocator
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     ev0.record()
-    counts = pipe.count_epoch(sched, 0)
+    counts = pipe.count_epoch(sched, 0, shared=share_plan)
     ev1.record()
     torch.cuda.synchronize()
     plan_ms = ev0.elapsed_time(ev1)
+    plan_shared_exact = bool(torch.equal(counts, counts_local)) if share_plan else None
+    del counts_local
     _, nout, hist, bm = candidates(counts, store.owner, part, nb)
     n_remote = int(nout.item())
     n_hot = resolve_n_hot(args.cache_pct, n_remote)
@@ -738,9 +743,14 @@ def main():
         check["shared_sampling_bit_exact"] = shared_check
     if check is not None and pin is not None:
         check["structure_pinned"] = pin
+    if check is not None and plan_shared_exact is not None:
+        # the epoch's access table from 1/N of the groups per rank + an
+        # all-reduce equals the table of a full local plan pass
+        check["plan_pass_shared_bit_exact"] = plan_shared_exact
     if check is not None and world > 1:
         flags = torch.tensor([int(check["blocks_bit_exact"] and check["rows_bit_exact"]
-                                  and check.get("shared_sampling_bit_exact", True))],
+                                  and check.get("shared_sampling_bit_exact", True)
+                                  and check.get("plan_pass_shared_bit_exact", True))],
                              device="cuda")
         dist.all_reduce(flags, op=dist.ReduceOp.MIN)
         check["all_ranks_bit_exact"] = bool(flags.item())

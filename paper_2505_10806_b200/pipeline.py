@@ -383,9 +383,21 @@ class WorkerPipeline:
         return out[: req.numel()]
 
     # -- per epoch ---------------------------------------------------------
-    def count_epoch(self, schedule: SeedSchedule, e: int) -> torch.Tensor:
+    def count_epoch(self, schedule: SeedSchedule, e: int, shared: bool = False) -> torch.Tensor:
+        """Access counts of every node over epoch e (collect_access,
+        plan.py:108-130; worker-independent, the remote mask is applied at
+        extraction).  shared (N > 1, torch.distributed up): each rank samples
+        every N-th group and one NCCL all-reduce sums the integer counts —
+        the same table on every rank, 1/N of the sampling."""
         counts = torch.zeros(self.dg.n, dtype=I32, device=self.dg.device)
-        self.plan.run_epoch(schedule, e, counts)
+        world = getattr(self, "world", 1) if shared else 1
+        if world > 1:
+            import torch.distributed as dist
+
+            self.plan.run_epoch(schedule, e, counts, share=(self.rank, world))
+            dist.all_reduce(counts)
+        else:
+            self.plan.run_epoch(schedule, e, counts)
         return counts
 
     def select_hot(self, counts: torch.Tensor, n_hot: int, max_count: int) -> torch.Tensor:

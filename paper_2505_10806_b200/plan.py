@@ -110,12 +110,15 @@ class PlanPass:
                   _lib.stream_handle())
 
     def run_epoch(self, schedule: SeedSchedule, e: int, counts: torch.Tensor,
-                  on_group=None) -> torch.Tensor:
+                  on_group=None, share: tuple[int, int] = (0, 1)) -> torch.Tensor:
         """Sample every batch of epoch e, add its input sets to counts.
-        on_group(i0, ng) is called after each group (for host consumers)."""
+        on_group(i0, ng) is called after each group (for host consumers).
+        share = (rank, world): only every world-th group from `rank` (the
+        caller sums the ranks' counts, e.g. one all-reduce)."""
         perm = self.permutation(schedule, e)
         smp, dg = self.sampler, self.dg
-        for i0 in range(0, self.nb, self.G):
+        rank, world = share
+        for i0 in range(rank * self.G, self.nb, world * self.G):
             ng = min(self.G, self.nb - i0)
             self.fill(perm, e, i0, ng)
             smp.run(ng)
